@@ -1,0 +1,203 @@
+"""float64 CPU oracle of the Polyglot window-LM SGD step -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and the ``cpu_baseline`` /
+``--impl reference`` legs of ``bench.py`` may import this package.  It shares
+nothing with the CUDA product path (``paper_1404_1521_b200``): the arithmetic
+lives in ``oracle/pgo.c`` (plain C, float64) and this module only marshals
+numpy arrays through ctypes.
+
+Parity pins for every function (none is "parity unpinned"):
+  * pgo_forward / pgo_score  -- closed forms (zero params -> loss 1; the
+    h=1 clamp case), one-hot dense brute force over a tiny
+    vocabulary, swap symmetry m -> 2 - m;
+  * pgo_backward             -- central finite differences of the loss in
+    float64, one-hot dense form of the embedding
+    gradient, saturation / inactive-hinge special cases;
+  * pgo_index_add(_f32)      -- SPEC.md:67-69 worked examples, the
+    10000-ones example, decomposability;
+  * pgo_train_step(_dp)      -- zero-params fixed point, b2 invariance,
+    locality, DP emulation == single step up to rounding;
+  * pgo_init_params          -- golden hash under tests/golden/ written by a
+    script that calls only this package, plus range/moment checks.
+See tests/test_oracle_*.py.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle_pg.so")
+_SRC = os.path.join(_HERE, "pgo.c")
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile pgo.c into liboracle_pg.so with plain gcc (no fast-math)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
+        os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "pgo.h"))
+    ):
+        tmp = _SO + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off",
+             "-o", tmp, _SRC, "-lm"]
+        )
+        os.replace(tmp, _SO)
+    return _SO
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        i64, i32, u64 = ctypes.c_int64, ctypes.c_int, ctypes.c_uint64
+        P = ctypes.c_void_p
+        L.pgo_init_params.argtypes = [i64, i32, i32, i32, u64, P, P, P, P, P]
+        L.pgo_forward.argtypes = [i64, i32, i32, i32, P, P, P, P, P, P, P, i64,
+                                  P, P, P, P, P]
+        L.pgo_backward.argtypes = [i64, i32, i32, i32, P, P, P, P, P, P, P, i64,
+                                   ctypes.c_double, P, P, P, P, P, P, P]
+        L.pgo_score.argtypes = [i64, i32, i32, i32, P, P, P, P, P, P, i64, P]
+        L.pgo_train_step.argtypes = [i64, i32, i32, i32, P, P, P, P, P, P, P,
+                                     i64, ctypes.c_double, P]
+        L.pgo_train_step_dp.argtypes = [i64, i32, i32, i32, P, P, P, P, P, P, P,
+                                        i64, i32, ctypes.c_double, P]
+        L.pgo_index_add.argtypes = [P, i64, i32, P, P, i64]
+        L.pgo_index_add_f32.argtypes = [P, i64, i32, P, P, i64]
+        L.pgo_last_bad.argtypes = [P, P]
+        for f in ("pgo_init_params", "pgo_forward", "pgo_backward", "pgo_score",
+                  "pgo_train_step", "pgo_train_step_dp", "pgo_index_add",
+                  "pgo_index_add_f32"):
+            getattr(L, f).restype = ctypes.c_int
+        L.pgo_last_bad.restype = None
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(msg)
+        self.status = status
+
+
+def _check(rc, what):
+    if rc != 0:
+        pos, val = ctypes.c_int64(), ctypes.c_int64()
+        lib().pgo_last_bad(ctypes.byref(pos), ctypes.byref(val))
+        extra = f" (position {pos.value}, value {val.value})" if rc == 2 else ""
+        raise OracleError(rc, f"{what} failed with status {rc}{extra}")
+
+
+class Params:
+    """Model parameters theta = (C, W1, b1, w2, b2) in float64."""
+
+    def __init__(self, V, d, n, h, C=None, W1=None, b1=None, w2=None, b2=0.0):
+        self.V, self.d, self.n, self.h = int(V), int(d), int(n), int(h)
+        self.C = np.zeros((V, d)) if C is None else np.array(C, dtype=np.float64).reshape(V, d)
+        self.W1 = np.zeros((n * d, h)) if W1 is None else np.array(W1, dtype=np.float64).reshape(n * d, h)
+        self.b1 = np.zeros(h) if b1 is None else np.array(b1, dtype=np.float64).reshape(h)
+        self.w2 = np.zeros(h) if w2 is None else np.array(w2, dtype=np.float64).reshape(h)
+        self.b2 = np.array([float(b2)], dtype=np.float64)
+
+    @classmethod
+    def init(cls, V, d, n, h, seed):
+        p = cls(V, d, n, h)
+        _check(lib().pgo_init_params(V, d, n, h, seed, _p(p.C), _p(p.W1), _p(p.b1),
+                                     _p(p.w2), _p(p.b2)), "pgo_init_params")
+        return p
+
+    def copy(self):
+        return Params(self.V, self.d, self.n, self.h, self.C.copy(), self.W1.copy(),
+                      self.b1.copy(), self.w2.copy(), float(self.b2[0]))
+
+    def _args(self):
+        return (self.V, self.d, self.n, self.h, _p(self.C), _p(self.W1), _p(self.b1),
+                _p(self.w2), _p(self.b2))
+
+    def flat(self):
+        return np.concatenate([self.C.ravel(), self.W1.ravel(), self.b1, self.w2, self.b2])
+
+
+def forward(p: Params, idx, corr):
+    idx, corr = _i32(idx), _i32(corr)
+    B = corr.shape[0]
+    a = np.zeros((B, p.h)); ac = np.zeros((B, p.h))
+    s = np.zeros(B); sc = np.zeros(B); loss = np.zeros(1)
+    _check(lib().pgo_forward(*p._args(), _p(idx), _p(corr), B, _p(a), _p(ac), _p(s),
+                             _p(sc), _p(loss)), "pgo_forward")
+    return dict(a=a, a_corr=ac, s=s, s_corr=sc, loss=float(loss[0]))
+
+
+def loss(p: Params, idx, corr) -> float:
+    idx, corr = _i32(idx), _i32(corr)
+    out = np.zeros(1)
+    _check(lib().pgo_forward(*p._args(), _p(idx), _p(corr), corr.shape[0], None, None,
+                             None, None, _p(out)), "pgo_forward")
+    return float(out[0])
+
+
+def backward(p: Params, idx, corr, inv_batch=None):
+    idx, corr = _i32(idx), _i32(corr)
+    B = corr.shape[0]
+    inv = 1.0 / B if inv_batch is None else float(inv_batch)
+    dW1 = np.zeros_like(p.W1); db1 = np.zeros(p.h); dw2 = np.zeros(p.h); db2 = np.zeros(1)
+    rows = np.zeros(2 * p.n * B, dtype=np.int32)
+    Y = np.zeros((2 * p.n * B, p.d))
+    nrows = ctypes.c_int64()
+    _check(lib().pgo_backward(*p._args(), _p(idx), _p(corr), B, inv, _p(dW1), _p(db1),
+                              _p(dw2), _p(db2), _p(rows), _p(Y), ctypes.byref(nrows)),
+           "pgo_backward")
+    r = nrows.value
+    return dict(dW1=dW1, db1=db1, dw2=dw2, db2=float(db2[0]), rows=rows[:r], Y=Y[:r])
+
+
+def score(p: Params, idx):
+    idx = _i32(idx)
+    B = idx.shape[0]
+    out = np.zeros(B)
+    _check(lib().pgo_score(*p._args(), _p(idx), B, _p(out)), "pgo_score")
+    return out
+
+
+def train_step(p: Params, idx, corr, lr) -> float:
+    """In-place SGD step on p; returns the pre-update mean loss."""
+    idx, corr = _i32(idx), _i32(corr)
+    out = np.zeros(1)
+    _check(lib().pgo_train_step(*p._args(), _p(idx), _p(corr), corr.shape[0], float(lr),
+                                _p(out)), "pgo_train_step")
+    return float(out[0])
+
+
+def train_step_dp(p: Params, idx, corr, lr, world) -> float:
+    idx, corr = _i32(idx), _i32(corr)
+    out = np.zeros(1)
+    _check(lib().pgo_train_step_dp(*p._args(), _p(idx), _p(corr), corr.shape[0],
+                                   int(world), float(lr), _p(out)), "pgo_train_step_dp")
+    return float(out[0])
+
+
+def index_add(W, Y, I):
+    """Serial W[I[k]] += Y[k] for k in order; W mutated in place."""
+    I = _i32(I)
+    if W.dtype == np.float32:
+        Y = np.ascontiguousarray(Y, dtype=np.float32)
+        _check(lib().pgo_index_add_f32(_p(W), W.shape[0], W.shape[1], _p(Y), _p(I),
+                                       I.shape[0]), "pgo_index_add_f32")
+    else:
+        Y = np.ascontiguousarray(Y, dtype=np.float64)
+        _check(lib().pgo_index_add(_p(W), W.shape[0], W.shape[1], _p(Y), _p(I),
+                                   I.shape[0]), "pgo_index_add")
+    return W
