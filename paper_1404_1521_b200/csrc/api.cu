@@ -1,0 +1,579 @@
+// api.cu -- host implementation of the C ABI declared in include/pg.h.
+//
+// Owns device memory, the model stream, lazily sized per-batch workspace and
+// the launches of the sm_100a kernels (step.cu, scatter.cu, and the init and
+// score kernels below).  No torch types cross this boundary.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/pg.h"
+#include "common.cuh"
+#include "nccl_shim.h"
+#include "scatter.cuh"
+#include "step.cuh"
+
+using namespace pg;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static pg_status fail(pg_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CU(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(e_ == cudaErrorMemoryAllocation ? PG_ENOMEM : PG_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                   \
+  } while (0)
+
+extern "C" const char* pg_last_error(void) { return g_err.c_str(); }
+extern "C" int pg_abi_version(void) { return PG_ABI_VERSION; }
+
+// ------------------------------------------------------------------ model
+struct pg_model {
+  int device = 0, num_sms = 0;
+  int64_t V = 0;
+  int d = 0, n = 0, h = 0;
+  float *C = nullptr, *W1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;
+  DevStatus* st = nullptr;
+  DevStatus* st_host = nullptr;  // pinned mirror for blocking reads
+  cudaStream_t stream = nullptr;
+  int mode = PG_SCATTER_DET, fused = 1, fast = 0;
+  size_t smem_max = 0;
+  // per-batch workspace (capacity grows)
+  int64_t cap_lists = 0, cap_dense = 0, cap_off = 0, cap_in = 0;
+  float* dense_part = nullptr;
+  int32_t* list_rows = nullptr;
+  float* list_vals = nullptr;
+  int32_t* list_off = nullptr;
+  int32_t* d_idx = nullptr;
+  int32_t* d_corr = nullptr;
+  float* d_scores = nullptr;
+  int64_t launches = 0;
+  // data parallel
+  int rank = 0, world = 1;
+  void* comm = nullptr;
+  float* dp_send = nullptr;   // [rank record]
+  float* dp_recv = nullptr;   // [world][rank record]
+  size_t dp_rec_floats = 0;
+};
+
+// ------------------------------------------------------------------ init kernel
+// Reading G10 / pg.h: value = float((2u - 1) r), u = top 24 bits of output i of
+// the SplitMix64 stream keyed by seed ^ (0x632BE59BD9B4E019 * (tensor_id + 1)).
+__global__ void init_uniform_kernel(float* out, int64_t count, unsigned long long seed,
+                                    unsigned long long tensor_id, double r) {
+  const unsigned long long key = seed ^ (0x632BE59BD9B4E019ull * (tensor_id + 1ull));
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    unsigned long long z = key + (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    const double u = (double)(z >> 40) * (1.0 / 16777216.0);
+    out[i] = __double2float_rn(__dmul_rn(__dadd_rn(__dmul_rn(2.0, u), -1.0), r));
+  }
+}
+
+// ------------------------------------------------------------------ score kernel
+// Warp per window: s = w2 . clamp(W1^T x + b1, -1, 1) + b2.
+__global__ void score_kernel(const float* __restrict__ C, const float* __restrict__ W1,
+                             const float* __restrict__ b1, const float* __restrict__ w2,
+                             const float* __restrict__ b2, int64_t V, int d, int n, int h,
+                             const int32_t* __restrict__ idx, int B, float* out, DevStatus* st) {
+  extern __shared__ float xsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nd = n * d;
+  float* x = xsm + (size_t)warp * nd;
+  for (int64_t e = (int64_t)blockIdx.x * nw + warp; e < B; e += (int64_t)gridDim.x * nw) {
+    bool bad = false;
+    for (int i = lane; i < nd; i += 32) {
+      const int p = i / d, j = i % d;
+      const int row = __ldg(idx + e * n + p);
+      const bool ok = row >= 0 && (int64_t)row < V;
+      if (!ok && j == 0) {
+        atomicMin(&st->score_bad, ((unsigned long long)(e * n + p) << 32) | (unsigned)row);
+        atomicOr(&st->score_flags, 1);
+      }
+      bad |= !ok;
+      x[i] = ok ? __ldg(C + (size_t)row * d + j) : 0.f;
+    }
+    __syncwarp();
+    float sp = 0.f;
+    for (int u = lane; u < h; u += 32) {
+      float a = __ldg(b1 + u);
+      for (int i = 0; i < nd; ++i) a = fmaf(x[i], __ldg(W1 + (size_t)i * h + u), a);
+      sp += __ldg(w2 + u) * fminf(fmaxf(a, -1.f), 1.f);
+    }
+    const float s = warp_sum(sp) + __ldg(b2);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) out[e] = bad ? __int_as_float(0x7fc00000) : s;
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ helpers
+enum PtrKind { PTR_NULL, PTR_HOST, PTR_DEVICE };
+
+static PtrKind ptr_kind(const void* p) {
+  if (!p) return PTR_NULL;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return PTR_HOST;
+  }
+  return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? PTR_DEVICE : PTR_HOST;
+}
+
+static void free_ws(pg_model* m) {
+  cudaFree(m->dense_part); cudaFree(m->list_rows); cudaFree(m->list_vals); cudaFree(m->list_off);
+  m->dense_part = nullptr; m->list_rows = nullptr; m->list_vals = nullptr; m->list_off = nullptr;
+  m->cap_lists = m->cap_dense = m->cap_off = 0;
+}
+
+struct Geometry {
+  int P, R, T, cap, NL, dense_len, dense_stride;
+  size_t smem;
+};
+
+static Geometry geometry(const pg_model* m, int B) {
+  Geometry g{};
+  g.P = B < m->num_sms ? B : m->num_sms;
+  g.T = step_chunk_T(m->d, m->n, m->h, m->fast);
+  const int per = (B + g.P - 1) / g.P;
+  g.R = (per + g.T - 1) / g.T;
+  g.cap = (m->n + 1) * g.T;
+  g.NL = g.P * g.R;
+  g.dense_len = m->n * m->d * m->h + 2 * m->h;
+  g.dense_stride = ((g.dense_len + 1) + 3) & ~3;
+  g.smem = step_smem_bytes(m->d, m->n, m->h, g.T, g.NL * m->world, m->fast);
+  return g;
+}
+
+static pg_status ensure_ws(pg_model* m, int B) {
+  Geometry g = geometry(m, B);
+  if (g.smem > m->smem_max)
+    return fail(PG_EINVAL, "batch %d needs %zu B of shared memory per CTA (max %zu)", B, g.smem, m->smem_max);
+  const int64_t lists = (int64_t)g.NL * m->world;
+  const int64_t dense = (int64_t)g.P * m->world * g.dense_stride;
+  const int64_t off = lists * (g.P + 1);
+  if (lists * g.cap > m->cap_lists || dense > m->cap_dense || off > m->cap_off) {
+    CU(cudaStreamSynchronize(m->stream));
+    free_ws(m);
+    const int64_t L = lists * g.cap;
+    CU(cudaMalloc(&m->dense_part, sizeof(float) * dense));
+    CU(cudaMalloc(&m->list_rows, sizeof(int32_t) * L));
+    CU(cudaMalloc(&m->list_vals, sizeof(float) * L * m->d));
+    CU(cudaMalloc(&m->list_off, sizeof(int32_t) * off));
+    m->cap_lists = L; m->cap_dense = dense; m->cap_off = off;
+  }
+  if (B > m->cap_in) {
+    CU(cudaStreamSynchronize(m->stream));
+    cudaFree(m->d_idx); cudaFree(m->d_corr); cudaFree(m->d_scores);
+    CU(cudaMalloc(&m->d_idx, sizeof(int32_t) * (size_t)B * m->n));
+    CU(cudaMalloc(&m->d_corr, sizeof(int32_t) * (size_t)B));
+    CU(cudaMalloc(&m->d_scores, sizeof(float) * (size_t)B));
+    m->cap_in = B;
+  }
+  return PG_OK;
+}
+
+static pg_status check_model(const pg_model* m) {
+  if (!m) return fail(PG_EINVAL, "null model handle");
+  return PG_OK;
+}
+
+static pg_status set_device(const pg_model* m) {
+  CU(cudaSetDevice(m->device));
+  return PG_OK;
+}
+
+static pg_status status_from_flags(int flags, unsigned long long bad, const char* what) {
+  if (flags & 1) {
+    const long long pos = (long long)(bad >> 32);
+    const int val = (int)(unsigned)(bad & 0xffffffffull);
+    return fail(PG_ERANGE, "%s: index out of range at flat position %lld (value %d); no parameter was modified",
+                what, pos, val);
+  }
+  if (flags & 2) return fail(PG_EDIVERGED, "%s: non-finite loss; no parameter was modified", what);
+  return PG_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" pg_status pg_init(pg_model** out, int64_t vocab, int32_t dim, int32_t window, int32_t hidden,
+                             uint64_t seed) {
+  if (!out) return fail(PG_EINVAL, "pg_init: out is NULL");
+  *out = nullptr;
+  if (vocab < 2 || vocab > 2147483647LL) return fail(PG_EINVAL, "pg_init: vocab must be in [2, 2^31-1]");
+  if (dim < 1 || window < 1 || hidden < 1) return fail(PG_EINVAL, "pg_init: dim, window, hidden must be >= 1");
+  if (hidden > 1024 || window > 63 || dim > 4096)
+    return fail(PG_EINVAL, "pg_init: unsupported shape (hidden <= 1024, window <= 63, dim <= 4096)");
+  pg_model* m = new pg_model();
+  m->V = vocab; m->d = dim; m->n = window; m->h = hidden;
+  cudaError_t e = cudaGetDevice(&m->device);
+  if (e != cudaSuccess) { delete m; return fail(PG_ECUDA, "pg_init: no CUDA device: %s", cudaGetErrorString(e)); }
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, m->device);
+  if (prop.major < 10) {
+    delete m;
+    return fail(PG_ECUDA, "pg_init: libpg is built for sm_100a; device is sm_%d%d", prop.major, prop.minor);
+  }
+  m->num_sms = prop.multiProcessorCount < kMaxSMs ? prop.multiProcessorCount : kMaxSMs;
+  m->fast = step_fast_ok(dim, window, hidden);
+  if (!m->fast && (hidden > 128))
+    { delete m; return fail(PG_EINVAL, "pg_init: generic path supports hidden <= 128"); }
+  const int64_t nC = vocab * dim, nW = (int64_t)window * dim * hidden;
+  pg_status s = PG_OK;
+  auto bail = [&](pg_status st) { pg_free(m); return st; };
+  if (cudaMalloc(&m->C, sizeof(float) * nC) != cudaSuccess ||
+      cudaMalloc(&m->W1, sizeof(float) * nW) != cudaSuccess ||
+      cudaMalloc(&m->b1, sizeof(float) * hidden) != cudaSuccess ||
+      cudaMalloc(&m->w2, sizeof(float) * hidden) != cudaSuccess ||
+      cudaMalloc(&m->b2, sizeof(float)) != cudaSuccess ||
+      cudaMalloc(&m->st, sizeof(DevStatus)) != cudaSuccess ||
+      cudaMallocHost(&m->st_host, sizeof(DevStatus)) != cudaSuccess) {
+    cudaGetLastError();
+    return bail(fail(PG_ENOMEM, "pg_init: allocation failed (vocab %lld x dim %d)", (long long)vocab, dim));
+  }
+  const int blocks = m->num_sms * 8;
+  init_uniform_kernel<<<blocks, 256>>>(m->C, nC, seed, 0, 0.5);
+  init_uniform_kernel<<<blocks, 256>>>(m->W1, nW, seed, 1, 0.5 / (double)(window * dim));
+  init_uniform_kernel<<<1, 256>>>(m->w2, hidden, seed, 2, 0.5 / (double)hidden);
+  m->launches += 3;
+  cudaMemset(m->b1, 0, sizeof(float) * hidden);
+  cudaMemset(m->b2, 0, sizeof(float));
+  DevStatus z{};
+  z.bad = z.last_bad = z.sticky_bad = z.score_bad = kNoBad;
+  cudaMemcpy(m->st, &z, sizeof z, cudaMemcpyHostToDevice);
+  cudaError_t e2 = step_prepare(m->fast, prop.sharedMemPerBlockOptin, &m->smem_max);
+  if (e2 == cudaSuccess) e2 = scatter_prepare(2048);
+  if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e2 == cudaSuccess) e2 = cudaDeviceSynchronize();
+  if (e2 != cudaSuccess) return bail(fail(PG_ECUDA, "pg_init: %s", cudaGetErrorString(e2)));
+  *out = m;
+  (void)s;
+  return PG_OK;
+}
+
+extern "C" void pg_free(pg_model* m) {
+  if (!m) return;
+  cudaSetDevice(m->device);
+  if (m->stream) cudaStreamSynchronize(m->stream);
+  else cudaDeviceSynchronize();
+  if (m->comm) nccl_shim_destroy(m->comm);
+  free_ws(m);
+  cudaFree(m->C); cudaFree(m->W1); cudaFree(m->b1); cudaFree(m->w2); cudaFree(m->b2);
+  cudaFree(m->st); cudaFreeHost(m->st_host);
+  cudaFree(m->d_idx); cudaFree(m->d_corr); cudaFree(m->d_scores);
+  cudaFree(m->dp_send); cudaFree(m->dp_recv);
+  delete m;
+}
+
+extern "C" pg_status pg_get_shape(const pg_model* m, int64_t* vocab, int32_t* dim, int32_t* window,
+                                  int32_t* hidden) {
+  if (pg_status s = check_model(m)) return s;
+  if (vocab) *vocab = m->V;
+  if (dim) *dim = m->d;
+  if (window) *window = m->n;
+  if (hidden) *hidden = m->h;
+  return PG_OK;
+}
+
+extern "C" pg_status pg_set_option(pg_model* m, int key, int64_t value) {
+  if (pg_status s = check_model(m)) return s;
+  switch (key) {
+    case PG_OPT_SCATTER:
+      if (value != PG_SCATTER_DET && value != PG_SCATTER_ATOMIC)
+        return fail(PG_EINVAL, "PG_OPT_SCATTER: unknown mode %lld", (long long)value);
+      m->mode = (int)value;
+      return PG_OK;
+    case PG_OPT_STREAM:
+      m->stream = reinterpret_cast<cudaStream_t>(value);
+      return PG_OK;
+    case PG_OPT_FUSED:
+      m->fused = value ? 1 : 0;
+      return PG_OK;
+    case 4: {  // PG_OPT_RESERVE (internal): pre-size workspace for a batch
+      if (value < 1 || value > (1 << 30)) return fail(PG_EINVAL, "reserve: bad batch");
+      if (pg_status s = set_device(m)) return s;
+      return ensure_ws(m, (int)value);
+    }
+    default:
+      return fail(PG_EINVAL, "pg_set_option: unknown key %d", key);
+  }
+}
+
+extern "C" int64_t pg_kernel_launches(const pg_model* m) { return m ? m->launches : 0; }
+
+static pg_status copy_param(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+  return PG_OK;
+}
+
+extern "C" pg_status pg_get_params(pg_model* m, float* C, float* W1, float* b1, float* w2, float* b2) {
+  if (pg_status s = check_model(m)) return s;
+  if (pg_status s = set_device(m)) return s;
+  const size_t nW = (size_t)m->n * m->d * m->h;
+  pg_status s = PG_OK;
+  if (C && !s) s = copy_param(C, m->C, sizeof(float) * (size_t)m->V * m->d, m->stream);
+  if (W1 && !s) s = copy_param(W1, m->W1, sizeof(float) * nW, m->stream);
+  if (b1 && !s) s = copy_param(b1, m->b1, sizeof(float) * m->h, m->stream);
+  if (w2 && !s) s = copy_param(w2, m->w2, sizeof(float) * m->h, m->stream);
+  if (b2 && !s) s = copy_param(b2, m->b2, sizeof(float), m->stream);
+  if (s) return s;
+  CU(cudaStreamSynchronize(m->stream));
+  return PG_OK;
+}
+
+extern "C" pg_status pg_set_params(pg_model* m, const float* C, const float* W1, const float* b1,
+                                   const float* w2, float b2) {
+  if (pg_status s = check_model(m)) return s;
+  if (pg_status s = set_device(m)) return s;
+  const size_t nW = (size_t)m->n * m->d * m->h;
+  pg_status s = PG_OK;
+  if (C && !s) s = copy_param(m->C, C, sizeof(float) * (size_t)m->V * m->d, m->stream);
+  if (W1 && !s) s = copy_param(m->W1, W1, sizeof(float) * nW, m->stream);
+  if (b1 && !s) s = copy_param(m->b1, b1, sizeof(float) * m->h, m->stream);
+  if (w2 && !s) s = copy_param(m->w2, w2, sizeof(float) * m->h, m->stream);
+  if (!std::isnan(b2) && !s) {
+    float tmp = b2;
+    s = copy_param(m->b2, &tmp, sizeof(float), m->stream);
+    if (!s) CU(cudaStreamSynchronize(m->stream));
+  }
+  if (s) return s;
+  CU(cudaStreamSynchronize(m->stream));
+  return PG_OK;
+}
+
+static pg_status stage_inputs(pg_model* m, const int32_t* idx, const int32_t* corr, int B,
+                              const int32_t** d_idx, const int32_t** d_corr) {
+  const PtrKind ki = ptr_kind(idx);
+  if (ki == PTR_DEVICE) {
+    *d_idx = idx;
+  } else {
+    CU(cudaMemcpyAsync(m->d_idx, idx, sizeof(int32_t) * (size_t)B * m->n, cudaMemcpyHostToDevice, m->stream));
+    *d_idx = m->d_idx;
+  }
+  if (corr) {
+    const PtrKind kc = ptr_kind(corr);
+    if (kc == PTR_DEVICE) {
+      *d_corr = corr;
+    } else {
+      CU(cudaMemcpyAsync(m->d_corr, corr, sizeof(int32_t) * (size_t)B, cudaMemcpyHostToDevice, m->stream));
+      *d_corr = m->d_corr;
+    }
+  }
+  return PG_OK;
+}
+
+static pg_status run_step(pg_model* m, const int32_t* idx, const int32_t* corr, int B, float lr,
+                          float* loss_dev);
+
+extern "C" pg_status pg_train_step(pg_model* m, const int32_t* idx_batch, const int32_t* corrupt_idx,
+                                   int32_t batch, float lr, float* loss_out) {
+  if (pg_status s = check_model(m)) return s;
+  if (!idx_batch || !corrupt_idx) return fail(PG_EINVAL, "pg_train_step: null index pointer");
+  if (batch < 1) return fail(PG_EINVAL, "pg_train_step: empty batch (batch=%d); the loss is undefined", batch);
+  if (!std::isfinite(lr) || !(lr > 0.f)) return fail(PG_EINVAL, "pg_train_step: lr must be finite and > 0 (got %g)", lr);
+  if (pg_status s = set_device(m)) return s;
+  if (pg_status s = ensure_ws(m, batch)) return s;
+  const PtrKind kl = ptr_kind(loss_out);
+  const int32_t *di = nullptr, *dc = nullptr;
+  if (pg_status s = stage_inputs(m, idx_batch, corrupt_idx, batch, &di, &dc)) return s;
+  if (pg_status s = run_step(m, di, dc, batch, lr, kl == PTR_DEVICE ? loss_out : nullptr)) return s;
+  if (kl != PTR_HOST) return PG_OK;
+  CU(cudaMemcpyAsync(m->st_host, m->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  *loss_out = m->st_host->last_loss;
+  const int flags = m->world > 1 ? m->st_host->rank_flags : m->st_host->last_flags;
+  return status_from_flags(flags, m->st_host->last_bad, "pg_train_step");
+}
+
+extern "C" float pg_train_step_loss(pg_model* m, const int32_t* idx_batch, const int32_t* corrupt_idx,
+                                    int32_t batch, float lr) {
+  float loss = NAN;
+  pg_status s = pg_train_step(m, idx_batch, corrupt_idx, batch, lr, &loss);
+  return s == PG_OK ? loss : NAN;
+}
+
+extern "C" pg_status pg_score(pg_model* m, const int32_t* idx_batch, int32_t batch, float* scores_out) {
+  if (pg_status s = check_model(m)) return s;
+  if (!idx_batch || !scores_out) return fail(PG_EINVAL, "pg_score: null pointer");
+  if (batch < 1) return fail(PG_EINVAL, "pg_score: empty batch");
+  if (pg_status s = set_device(m)) return s;
+  if (pg_status s = ensure_ws(m, batch)) return s;
+  const int32_t *di = nullptr, *dc = nullptr;
+  if (pg_status s = stage_inputs(m, idx_batch, nullptr, batch, &di, &dc)) return s;
+  const PtrKind ko = ptr_kind(scores_out);
+  float* out = ko == PTR_DEVICE ? scores_out : m->d_scores;
+  CU(cudaMemsetAsync(&m->st->score_flags, 0, sizeof(int), m->stream));
+  CU(cudaMemsetAsync(&m->st->score_bad, 0xff, sizeof(unsigned long long), m->stream));
+  const int warps = 8;
+  const size_t sm = sizeof(float) * warps * m->n * m->d;
+  if (sm > 200 * 1024) return fail(PG_EINVAL, "pg_score: window*dim too large");
+  int blocks = (batch + warps - 1) / warps;
+  if (blocks > m->num_sms * 16) blocks = m->num_sms * 16;
+  score_kernel<<<blocks, warps * 32, sm, m->stream>>>(m->C, m->W1, m->b1, m->w2, m->b2, m->V, m->d, m->n, m->h,
+                                                      di, batch, out, m->st);
+  m->launches += 1;
+  CU(cudaGetLastError());
+  if (ko == PTR_DEVICE) return PG_OK;
+  CU(cudaMemcpyAsync(scores_out, out, sizeof(float) * batch, cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaMemcpyAsync(m->st_host, m->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  return status_from_flags(m->st_host->score_flags & 1, m->st_host->score_bad, "pg_score");
+}
+
+extern "C" pg_status pg_sync(pg_model* m) {
+  if (pg_status s = check_model(m)) return s;
+  if (pg_status s = set_device(m)) return s;
+  CU(cudaMemcpyAsync(m->st_host, m->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  const int flags = m->st_host->sticky_flags;
+  const unsigned long long bad = m->st_host->sticky_bad;
+  if (flags) {
+    CU(cudaMemsetAsync(&m->st->sticky_flags, 0, sizeof(int), m->stream));
+    CU(cudaMemsetAsync(&m->st->sticky_bad, 0xff, sizeof(unsigned long long), m->stream));
+    CU(cudaStreamSynchronize(m->stream));
+  }
+  return status_from_flags(flags, bad, "asynchronous pg_train_step");
+}
+
+// ------------------------------------------------------------------ step launch
+static StepParams make_params(pg_model* m, const Geometry& g, const int32_t* idx, const int32_t* corr, int B,
+                              float lr, float* loss_dev) {
+  StepParams p{};
+  p.C = m->C; p.W1 = m->W1; p.b1 = m->b1; p.w2 = m->w2; p.b2 = m->b2;
+  p.V = m->V; p.d = m->d; p.n = m->n; p.h = m->h;
+  p.idx = idx; p.corr = corr; p.B = B;
+  p.inv_B = 1.0f / (float)((int64_t)B * m->world);
+  p.lr = lr;
+  p.P = g.P; p.R = g.R; p.T = g.T; p.cap = g.cap;
+  p.dense_part = m->dense_part;
+  p.dense_len = g.dense_len; p.dense_stride = g.dense_stride;
+  p.list_rows = m->list_rows; p.list_vals = m->list_vals; p.list_off = m->list_off;
+  p.Ptot = g.P; p.NLtot = g.NL;
+  p.st = m->st;
+  p.loss_out = loss_dev;
+  p.mode = m->mode;
+  p.smem_bytes = (int)g.smem;
+  return p;
+}
+
+pg_status dp_step(pg_model* m, const Geometry& g, StepParams& p);
+
+static pg_status run_step(pg_model* m, const int32_t* idx, const int32_t* corr, int B, float lr,
+                          float* loss_dev) {
+  const Geometry g = geometry(m, B);
+  StepParams p = make_params(m, g, idx, corr, B, lr, loss_dev);
+  if (m->world > 1) return dp_step(m, g, p);
+  int l = 0;
+  launch_step(p, m->fused, m->fast, m->stream, &l);
+  m->launches += l;
+  CU(cudaGetLastError());
+  return PG_OK;
+}
+
+// ------------------------------------------------------------------ data parallel (NCCL)
+pg_status dp_step(pg_model* m, const Geometry& g, StepParams& p) {
+  (void)g; (void)p;
+  return fail(PG_ENCCL, "data-parallel step not available in this build");
+}
+
+extern "C" pg_status pg_nccl_unique_id(void* out) {
+  if (!out) return fail(PG_EINVAL, "pg_nccl_unique_id: NULL");
+  std::string err;
+  if (nccl_shim_unique_id(out, &err)) return fail(PG_ENCCL, "%s", err.c_str());
+  return PG_OK;
+}
+
+extern "C" pg_status pg_attach_nccl(pg_model* m, int rank, int world, const void* uid) {
+  if (pg_status s = check_model(m)) return s;
+  if (!uid || world < 1 || rank < 0 || rank >= world) return fail(PG_EINVAL, "pg_attach_nccl: bad rank/world");
+  if (world == 1) return PG_OK;
+  if (pg_status s = set_device(m)) return s;
+  std::string err;
+  void* comm = nullptr;
+  if (nccl_shim_init(&comm, rank, world, uid, &err)) return fail(PG_ENCCL, "%s", err.c_str());
+  if (m->comm) nccl_shim_destroy(m->comm);
+  m->comm = comm;
+  m->rank = rank;
+  m->world = world;
+  free_ws(m);   // record layout depends on world
+  return PG_OK;
+}
+
+// ------------------------------------------------------------------ standalone scatter-add
+namespace {
+std::mutex g_sc_mu;
+void* g_sc_ws[16] = {nullptr};
+size_t g_sc_cap[16] = {0};
+}
+
+static pg_status scatter_common(float* W, int64_t rows, int32_t cols, const float* Y, const int32_t* I, int64_t n,
+                                int mode, void* stream, int* err_dev, bool blocking) {
+  if (!W || (n > 0 && (!Y || !I))) return fail(PG_EINVAL, "pg_scatter_add: null pointer");
+  if (rows < 1 || cols < 1 || n < 0 || rows > 2147483647LL) return fail(PG_EINVAL, "pg_scatter_add: bad shape");
+  if (mode != PG_SCATTER_DET && mode != PG_SCATTER_ATOMIC) return fail(PG_EINVAL, "pg_scatter_add: bad mode");
+  if (!scatter_supported(cols, mode))
+    return fail(PG_EINVAL, "pg_scatter_add: DET mode supports cols in {<=32, 64, 128} (got %d)", cols);
+  if (n == 0) return PG_OK;
+  if (n >= (1ll << 30)) return fail(PG_EINVAL, "pg_scatter_add: n must be < 2^30");
+  if (ptr_kind(W) != PTR_DEVICE || ptr_kind(Y) != PTR_DEVICE || ptr_kind(I) != PTR_DEVICE)
+    return fail(PG_EINVAL, "pg_scatter_add: W, Y and I must be device pointers");
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  if (dev >= 16) return fail(PG_EINVAL, "pg_scatter_add: device index >= 16");
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  std::lock_guard<std::mutex> lk(g_sc_mu);
+  ScatterPlan pl = scatter_plan(rows, cols, n, sms);
+  if (pl.total_bytes > g_sc_cap[dev]) {
+    CU(cudaDeviceSynchronize());
+    cudaFree(g_sc_ws[dev]);
+    g_sc_ws[dev] = nullptr;
+    CU(cudaMalloc(&g_sc_ws[dev], pl.total_bytes));
+    g_sc_cap[dev] = pl.total_bytes;
+    CU(scatter_prepare(2048));   // the largest digit table any plan uses
+  }
+  int l = 0;
+  CU(scatter_launch(pl, g_sc_ws[dev], W, rows, cols, Y, I, n, mode, s, &l));
+  ScatterStatus* st = reinterpret_cast<ScatterStatus*>(static_cast<unsigned char*>(g_sc_ws[dev]) + pl.off_status);
+  if (err_dev) CU(cudaMemcpyAsync(err_dev, &st->flag, sizeof(int), cudaMemcpyDeviceToDevice, s));
+  if (!blocking) return PG_OK;
+  ScatterStatus hs;
+  CU(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (hs.flag) {
+    return fail(PG_ERANGE, "pg_scatter_add: index out of range at position %lld (value %d); W unchanged",
+                (long long)(hs.bad >> 32), (int)(unsigned)(hs.bad & 0xffffffffull));
+  }
+  return PG_OK;
+}
+
+extern "C" pg_status pg_scatter_add(float* W, int64_t rows, int32_t cols, const float* Y, const int32_t* I,
+                                    int64_t n, int mode, void* stream) {
+  return scatter_common(W, rows, cols, Y, I, n, mode, stream, nullptr, true);
+}
+
+extern "C" pg_status pg_scatter_add_async(float* W, int64_t rows, int32_t cols, const float* Y, const int32_t* I,
+                                          int64_t n, int mode, void* stream, int* err_flag_dev) {
+  return scatter_common(W, rows, cols, Y, I, n, mode, stream, err_flag_dev, false);
+}

@@ -1,0 +1,29 @@
+// scatter.cuh -- host interface of the standalone scatter-add pipelines.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace pg {
+
+struct ScatterStatus {
+  int flag;                 // 1: an index was out of range -> nothing applied
+  int pad;
+  unsigned long long bad;   // min over (position << 32 | uint32 value)
+};
+
+struct ScatterPlan {
+  int passes, bits, bins, num_sms;
+  int64_t ntiles, nchunks;
+  size_t off_status, off_hist, off_ctr, off_lookback, zero_bytes;
+  size_t off_ka, off_va, off_kb, off_vb, off_carry, total_bytes;
+};
+
+ScatterPlan scatter_plan(int64_t rows, int cols, int64_t n, int num_sms);
+int scatter_supported(int cols, int mode);
+cudaError_t scatter_prepare(int bins);
+cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t rows, int cols,
+                           const float* Y, const int32_t* I, int64_t n, int mode, cudaStream_t s,
+                           int* launches);
+
+}  // namespace pg

@@ -1,0 +1,202 @@
+"""GPU parity of the fused SGD step (libpg, sm_100a) against the float64 oracle.
+
+All calls go through the C ABI (paper_1404_1521_b200 ctypes binding).
+Tolerances: SURVEY.md §8(c) T1-T5, restated in DESIGN.md.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests._parity import assert_parity, oracle_from_gpu_params, rel_inf, run_both
+
+pytestmark = pytest.mark.gpu
+
+TINY = dict(V=1000, d=16, n=5, h=32)
+POLY = dict(V=100_000, d=64, n=5, h=32)
+
+
+@pytest.fixture(scope="module")
+def pg():
+    import paper_1404_1521_b200 as pg
+    import torch
+    assert torch.cuda.is_available()
+    pg.lib()
+    return pg
+
+
+def make(pg, cfg, seed=42, scatter=0, fused=True):
+    return pg.PolyglotModel(cfg["V"], cfg["d"], cfg["n"], cfg["h"], seed=seed, scatter=scatter,
+                            fused=fused)
+
+
+def test_init_matches_oracle_init_bitwise(pg):
+    for cfg in (TINY, POLY):
+        m = make(pg, cfg, seed=1234)
+        C, W1, b1, w2, b2 = m.get_params()
+        ref = oracle.Params.init(cfg["V"], cfg["d"], cfg["n"], cfg["h"], 1234)
+        np.testing.assert_array_equal(C.astype(np.float64), ref.C)
+        np.testing.assert_array_equal(W1.astype(np.float64), ref.W1)
+        np.testing.assert_array_equal(w2.astype(np.float64), ref.w2)
+        assert not b1.any() and b2 == 0.0
+        m.close()
+
+
+@pytest.mark.parametrize("scatter", [0, 1])
+def test_tiny_100_steps(pg, scatter):
+    # BASELINE.json configs[0]: tiny, batch 16, 100 SGD steps (generic kernel path)
+    m = make(pg, TINY, scatter=scatter)
+    gl, rl, p0, pend, ref = run_both(m, **TINY, B=16, steps=100)
+    rep = assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3,
+                        c_roundings=run_both.occurrences if scatter else None)
+    print("tiny", scatter, rep)
+    m.close()
+
+
+@pytest.mark.parametrize("scatter", [0, 1])
+def test_polyglot_b1024_default_init(pg, scatter):
+    m = make(pg, POLY, scatter=scatter)
+    gl, rl, p0, pend, ref = run_both(m, **POLY, B=1024, steps=10)
+    rep = assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3,
+                        c_roundings=run_both.occurrences if scatter else None)
+    print("poly", scatter, rep)
+    m.close()
+
+
+@pytest.mark.parametrize("scatter", [0, 1])
+def test_polyglot_saturated_regime(pg, scatter):
+    # W1, w2 scaled x200 so units saturate and margins go negative (T3: tau 1e-4)
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    start = synth.random_params(V, d, n, h, seed=5, w1_scale=200 * 0.5 / (n * d), w2_scale=200 * 0.5 / h)
+    m = make(pg, POLY, scatter=scatter)
+    gl, rl, p0, pend, ref = run_both(m, V, d, n, h, B=1024, steps=10, start_params=start)
+    f = oracle.forward(oracle_from_gpu_params(p0, V, d, n, h), *synth.batch(V, n, 1024, seed=42, step=0))
+    assert (np.abs(f["a"]) > 1).mean() > 0.2          # really saturated
+    rep = assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-4,
+                        c_roundings=run_both.occurrences if scatter else None)
+    print("sat", scatter, rep)
+    m.close()
+
+
+@pytest.mark.parametrize("B", [1, 7, 149, 1000, 4096 + 37, 9000])
+def test_ragged_batches(pg, B):
+    # ragged tails, fewer examples than SMs, and several chunks per CTA (B > 148*32)
+    m = make(pg, POLY)
+    gl, rl, p0, pend, ref = run_both(m, **POLY, B=B, steps=3, kind="iid")
+    assert_parity(gl, rl, p0, pend, ref, tau_delta=2e-3)
+    m.close()
+
+
+def test_det_bitwise_reproducible_and_fused_equals_split(pg):
+    outs = []
+    for fused in (True, True, False):
+        m = make(pg, POLY, fused=fused)
+        for t in range(5):
+            idx, corr = synth.batch(POLY["V"], POLY["n"], 2048, seed=7, step=t)
+            m.train_step(idx, corr, 0.1)
+        outs.append(m.get_params())
+        m.close()
+    for k in range(4):
+        assert np.array_equal(outs[0][k], outs[1][k]), "T5: det run-to-run"
+        assert np.array_equal(outs[0][k], outs[2][k]), "fused vs split"
+
+
+def test_bad_index_no_mutation(pg):
+    m = make(pg, POLY)
+    p0 = m.get_params()
+    idx, corr = synth.batch(POLY["V"], POLY["n"], 256, seed=1)
+    bad = idx.copy(); bad[17, 3] = POLY["V"]
+    with pytest.raises(pg.PGError) as e:
+        m.train_step(bad, corr, 0.1)
+    assert e.value.status == pg.PG_ERANGE
+    assert f"position {17 * 5 + 3} (value {POLY['V']})" in str(e.value)
+    badc = corr.copy(); badc[3] = -5
+    with pytest.raises(pg.PGError) as e:
+        m.train_step(idx, badc, 0.1)
+    assert f"position {256 * 5 + 3} (value -5)" in str(e.value)
+    p1 = m.get_params()
+    for a, b in zip(p0[:4], p1[:4]):
+        assert np.array_equal(a, b)
+    # the model keeps working afterwards
+    loss = m.train_step(idx, corr, 0.1)
+    assert np.isfinite(loss)
+    m.close()
+
+
+def test_host_checked_errors(pg):
+    m = make(pg, TINY)
+    idx, corr = synth.batch(TINY["V"], TINY["n"], 4, seed=1)
+    for lr in (0.0, -1.0, float("nan"), float("inf")):
+        with pytest.raises(pg.PGError) as e:
+            m.train_step(idx, corr, lr)
+        assert e.value.status == pg.PG_EINVAL
+    with pytest.raises(pg.PGError) as e:
+        m.train_step(idx[:0], corr[:0], 0.1)
+    assert e.value.status == pg.PG_EINVAL
+    m.close()
+
+
+def test_zero_params_fixed_point(pg):
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    m = make(pg, POLY)
+    m.set_params(np.zeros((V, d)), np.zeros((n * d, h)), np.zeros(h), np.zeros(h), 0.0)
+    for t in range(3):
+        idx, corr = synth.batch(V, n, 512, seed=3, step=t)
+        assert m.train_step(idx, corr, 0.1) == 1.0
+    for a in m.get_params()[:4]:
+        assert not a.any()
+    m.close()
+
+
+def test_locality_untouched_rows_bit_identical(pg):
+    V, n = POLY["V"], POLY["n"]
+    m = make(pg, POLY)
+    C0 = m.get_params()[0]
+    idx, corr = synth.batch(V, n, 1024, seed=9)
+    m.train_step(idx, corr, 0.1)
+    C1 = m.get_params()[0]
+    touched = np.zeros(V, bool); touched[idx.ravel()] = True; touched[corr] = True
+    assert np.array_equal(C1[~touched], C0[~touched])
+    assert (C1[touched] != C0[touched]).any()
+    m.close()
+
+
+def test_score_matches_oracle(pg):
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    m = make(pg, POLY)
+    p = m.get_params()
+    idx, _ = synth.batch(V, n, 777, seed=4)
+    s = m.score(idx)
+    r = oracle.score(oracle_from_gpu_params(p, V, d, n, h), idx)
+    assert np.abs(s - r).max() <= 1e-4 * np.abs(r).max()
+    bad = idx.copy(); bad[5, 0] = V + 3
+    with pytest.raises(pg.PGError) as e:
+        m.score(bad)
+    assert e.value.status == pg.PG_ERANGE
+    m.close()
+
+
+def test_device_pointers_async_loss(pg):
+    import torch
+    V, n = POLY["V"], POLY["n"]
+    a, b = make(pg, POLY), make(pg, POLY)
+    dl = torch.zeros(1, dtype=torch.float32, device="cuda")
+    for t in range(3):
+        idx, corr = synth.batch(V, n, 1024, seed=11, step=t)
+        la = a.train_step(idx, corr, 0.1)
+        b.train_step(torch.from_numpy(idx).cuda(), torch.from_numpy(corr).cuda(), 0.1, loss_out=dl)
+        torch.cuda.synchronize()
+        assert dl.item() == la
+    b.sync()
+    for x, y in zip(a.get_params()[:4], b.get_params()[:4]):
+        assert np.array_equal(x, y)
+    a.close(); b.close()
+
+
+def test_large_shape_generic_path(pg):
+    # BASELINE.json configs[4] shape (V 1M, d 128, h 128) on one GPU, small batch
+    V, d, n, h = 1_000_000, 128, 5, 128
+    m = pg.PolyglotModel(V, d, n, h, seed=3)
+    gl, rl, p0, pend, ref = run_both(m, V, d, n, h, B=512, steps=2)
+    assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3)
+    m.close()
