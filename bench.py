@@ -1,0 +1,377 @@
+"""Benchmark: Polyglot window-LM SGD steps/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path (gather, forward, hinge, backward,
+dense update, embedding scatter-add -- SURVEY.md §8(a) rows a1-a6) over one
+batch of synthetic Zipf windows (synth/).  Workload:
+BASELINE.json configs[1] (Polyglot V 100k, d 64, n 5, h 32) at batch 4096 per
+GPU (the top of its 16-4096 sweep).  Under torchrun (N > 1) the library runs
+data-parallel over NCCL with batch 4096 per rank (weak scaling).
+
+Timing: inputs for all steps are pre-staged in HBM; the L2 is flushed (512 MB
+write) before every timed step; each step is bracketed by CUDA events on the
+library's stream; value = examples / sum of step times, max over ranks.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+POLY = dict(V=100_000, d=64, n=5, h=32)
+FMA_PER_EXAMPLE = lambda d, n, h: (n * d * h) + d * h + ((n - 1) * d * h + 2 * d * h) + ((n + 1) * d * h)
+# forward (n*d*h + d*h for the corrupt centre) + gradient rows ((n-1)*d*h + 2*d*h)
+# + dW1 ((n+1)*d*h)  = 36,864 FMA = 73.7 kFLOP per example at the Polyglot shape
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=4096, help="examples per GPU per step")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scatter", choices=["det", "atomic"], default="det")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip sweep / scatter microbench")
+    ap.add_argument("--lr", type=float, default=0.1)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        import tempfile
+        self.path = tempfile.mktemp(prefix="pg_clocks_", suffix=".csv")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            try:
+                with open(self.path) as f:
+                    self.lines = [ln.strip() for ln in f if ln.strip()]
+                os.unlink(self.path)
+            except OSError:
+                pass
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        busy = sorted(sm)[len(sm) // 4:] or sm   # drop idle samples at the edges
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def fp32_alu_peak_tflops(sm_mhz, sms=148):
+    # 148 SMs x 4 SMSPs x 32 FP32 lanes x 2 FLOP/FMA x clock (B200_PROFILING.md /
+    # blackwell guide unit counts) -> 74.4 TFLOP/s at 1965 MHz
+    return sms * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+# ---------------------------------------------------------------------- oracle (reference arm / cpu baseline)
+def oracle_rate(B, steps, seed=42):
+    """The float64 oracle as it stands, single host thread, on `steps` Polyglot steps."""
+    import oracle
+    import synth
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    p = oracle.Params.init(V, d, n, h, seed)
+    batches = [synth.batch(V, n, B, seed=seed, step=t) for t in range(steps)]
+    t0 = time.perf_counter()
+    for idx, corr in batches:
+        oracle.train_step(p, idx, corr, 0.1)
+    dt = time.perf_counter() - t0
+    return B * steps / dt, dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    steps = max(1, min(args.steps, 20))
+    B = min(args.batch, 1024)
+    rate, dt = oracle_rate(B, steps)
+    cfg = {"workload": f"polyglot_v100k_d64_n5_h32_b{args.batch}", "vocab": POLY["V"], "dim": POLY["d"],
+           "window": POLY["n"], "hidden": POLY["h"], "batch_per_gpu": args.batch,
+           "oracle_sample": f"{steps} steps x batch {B}"}
+    print(json.dumps({
+        "impl": "reference", "metric": "training examples/sec", "value": rate, "unit": "examples/s",
+        "n_gpus": 0, "steps": steps, "warmup": 0, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": rate, "unit": "examples/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{steps} SGD steps of batch {B} (Polyglot shape), float64, 1 thread"},
+        "e2e": {"value": rate, "unit": "examples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1404_1521_b200 as pg
+    import synth
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    B = args.batch
+    stream = torch.cuda.Stream(device=dev)
+    model = pg.PolyglotModel(V, d, n, h, seed=42, scatter=1 if args.scatter == "atomic" else 0,
+                             stream=stream)
+    if world > 1:
+        uid = pg.pg_nccl_unique_id() if rank == 0 else bytes(128)
+        t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).to(dev)
+        dist.broadcast(t, 0)
+        model.attach_nccl(rank, world, bytes(t.cpu().numpy()))
+    model.reserve(B)
+    total = args.warmup + args.steps
+    # per-step synthetic batches, rank-specific substreams, resident in HBM
+    host = [synth.batch(V, n, B, seed=42 + 1000 * rank, step=t) for t in range(total)]
+    d_idx = [torch.from_numpy(i).to(dev) for i, _ in host]
+    d_corr = [torch.from_numpy(c).to(dev) for _, c in host]
+    loss_dev = torch.zeros(1, dtype=torch.float32, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    with torch.cuda.stream(stream):
+        for t in range(args.warmup):
+            model.train_step(d_idx[t], d_corr[t], args.lr, loss_out=loss_dev)
+    barrier()
+    model.sync()
+    l0 = model.kernel_launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                flush.zero_()                      # L2 flush, outside the timed region
+                ev[k][0].record(stream)
+                model.train_step(d_idx[args.warmup + k], d_corr[args.warmup + k], args.lr, loss_out=loss_dev)
+                ev[k][1].record(stream)
+        barrier()
+    launches = model.kernel_launches() - l0
+    model.sync()
+    times = [a.elapsed_time(b) for a, b in ev]          # ms
+    tot_ms = sum(times)
+    if world > 1:
+        tt = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tot_ms = float(tt.item())
+    ms_per_step = tot_ms / args.steps
+    value = B * world * args.steps / (tot_ms / 1e3)
+
+    # ---- warm-L2 steady state: K steps back to back (table stays L2-resident)
+    with torch.cuda.stream(stream):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for k in range(args.steps):
+            model.train_step(d_idx[args.warmup + k], d_corr[args.warmup + k], args.lr, loss_out=loss_dev)
+        e1.record(stream)
+    barrier()
+    warm_ms = e0.elapsed_time(e1) / args.steps
+
+    # ---- e2e through the public API with HOST buffers: pinned H2D of the
+    # step's inputs + blocking D2H of the loss/status, every step
+    pin_idx = [torch.from_numpy(i).pin_memory() for i, _ in host]
+    pin_corr = [torch.from_numpy(c).pin_memory() for _, c in host]
+    barrier()
+    with torch.cuda.stream(stream):
+        for k in range(min(3, total)):
+            model.train_step(pin_idx[k], pin_corr[k], args.lr)
+        barrier()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            model.train_step(pin_idx[args.warmup + k], pin_corr[args.warmup + k], args.lr)   # blocking
+        e2e_s = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e = {"value": B * world * args.steps / e2e_s, "unit": "examples/s",
+           "h2d_bytes_per_step": B * n * 4 + B * 4, "d2h_bytes_per_step": 80}
+
+    extras = {}
+    if not args.no_extras and rank == 0:
+        extras = run_extras(pg, torch, synth, np, dev, stream, flush, model)
+
+    if rank == 0:
+        peaks, peak_kind = measured_peaks()
+        clocks = clk.summary()
+        sm_max = clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        fma = FMA_PER_EXAMPLE(d, n, h)
+        flop_per_launch = 2.0 * fma * B
+        achieved = flop_per_launch / (ms_per_step / 1e3) / 1e12
+        peak = fp32_alu_peak_tflops(sm_max)
+        tr = load_traffic().get(f"step_b{B}")
+        out = {
+            "metric": "training examples/sec", "value": value, "unit": "examples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"polyglot_v100k_d64_n5_h32_b{B}", "vocab": V, "dim": d, "window": n,
+                       "hidden": h, "batch_per_gpu": B, "global_batch": B * world,
+                       "parallelism": f"dp{world}" if world > 1 else "single",
+                       "scatter": args.scatter, "l2": "flushed (512 MB write) before every timed step",
+                       "inputs": "Zipf(1) sliding windows + uniform corrupt centres, seed 42"},
+            "roofline": {"kernel": "pg::step_kernel<true> (fused cooperative step)", "bound": "alu",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": tr, "peak_source": f"FP32 FMA: 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz",
+                         "flop_per_example": 2 * fma},
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "l2_warm": {"value": B * world / (warm_ms / 1e3), "ms_per_step": warm_ms},
+            "peaks": {"source": peak_kind, "hbm_gbs": peaks.get("hbm_gbs")},
+        }
+        out.update(extras)
+        if not args.no_cpu_baseline:
+            rate, dt = oracle_rate(1024, 25)
+            out["cpu_baseline"] = {"value": rate, "unit": "examples/s", "cores": 1, "kind": "oracle",
+                                   "sample": "25 SGD steps x batch 1024 (Polyglot shape), float64, 1 host thread"}
+        print(json.dumps(out), flush=True)
+    model.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_extras(pg, torch, synth, np, dev, stream, flush, model):
+    """Batch sweep (configs[1]) and the scatter-add microbench (configs[2])."""
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    res = {}
+    sweep = {}
+    for B in (16, 64, 256, 1024, 2048, 4096, 8192):
+        model.reserve(B)
+        bs = [synth.batch(V, n, B, seed=7, step=t) for t in range(8)]
+        di = [torch.from_numpy(i).to(dev) for i, _ in bs]
+        dc = [torch.from_numpy(c).to(dev) for _, c in bs]
+        with torch.cuda.stream(stream):
+            for t in range(3):
+                model.train_step(di[t], dc[t], 0.1, loss_out=None)
+            torch.cuda.synchronize()
+            tms = []
+            for t in range(8):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                model.train_step(di[t], dc[t], 0.1, loss_out=None)
+                b.record(stream)
+                tms.append((a, b))
+            torch.cuda.synchronize()
+        ms = [a.elapsed_time(b) for a, b in tms]
+        sweep[str(B)] = {"us_per_step": 1e3 * statistics.mean(ms), "examples_per_s": B / (statistics.mean(ms) / 1e3)}
+    model.sync()
+    res["batch_sweep_l2_flushed"] = sweep
+    peaks, _ = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    sc = {}
+    rows, cols, N = 100_000, 64, 1_000_000
+    for dist_name in ("zipf", "uniform"):
+        I, Y = synth.scatter_inputs(rows, cols, N, dist_name, "random", seed=42)
+        U = int(np.unique(I).size)
+        alg_bytes = N * (4 * cols + 4) + 2 * U * 4 * cols
+        Id, Yd = torch.from_numpy(I).to(dev), torch.from_numpy(Y).to(dev)
+        W = torch.zeros(rows, cols, device=dev)
+        for mode_name, mode in (("det", 0), ("atomic", 1)):
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    pg.pg_scatter_add(W, Yd, Id, mode=mode, stream=stream)
+                tms = []
+                for _ in range(10):
+                    flush.zero_()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    pg.pg_scatter_add_async(W, Yd, Id, mode=mode, stream=stream)
+                    b.record(stream)
+                    tms.append((a, b))
+                torch.cuda.synchronize()
+            us = statistics.mean([a.elapsed_time(b) for a, b in tms]) * 1e3
+            gbs = alg_bytes / (us * 1e-6) / 1e9
+            sc[f"{dist_name}_{mode_name}"] = {"us": us, "achieved_gbs": gbs, "frac_of_hbm": gbs / hbm,
+                                              "algorithmic_bytes": alg_bytes, "unique_rows": U}
+    res["scatter_microbench"] = {"config": "100k x 64 fp32 table, 1M rows, L2 flushed, W[I]+=Y (pg_scatter_add)",
+                                 "peak_hbm_gbs": hbm, "results": sc}
+    return res
+
+
+if __name__ == "__main__":
+    main()

@@ -56,6 +56,7 @@ struct pg_model {
   cudaStream_t stream = nullptr;
   int mode = PG_SCATTER_DET, fused = 1, fast = 0;
   size_t smem_max = 0;
+  unsigned long long* trace = nullptr;
   // per-batch workspace (capacity grows)
   int64_t cap_lists = 0, cap_dense = 0, cap_off = 0, cap_in = 0;
   float* dense_part = nullptr;
@@ -150,6 +151,7 @@ static void free_ws(pg_model* m) {
 struct Geometry {
   int P, R, T, cap, NL, dense_len, dense_stride;
   size_t smem;
+  Layout lay;
 };
 
 static Geometry geometry(const pg_model* m, int B) {
@@ -162,7 +164,9 @@ static Geometry geometry(const pg_model* m, int B) {
   g.NL = g.P * g.R;
   g.dense_len = m->n * m->d * m->h + 2 * m->h;
   g.dense_stride = ((g.dense_len + 1) + 3) & ~3;
-  g.smem = step_smem_bytes(m->d, m->n, m->h, g.T, g.NL * m->world, m->fast);
+  g.lay = make_layout(m->d, m->n, m->h, g.T, step_block_threads(m->d, m->n, m->h, m->fast), g.NL * m->world,
+                      m->fast);
+  g.smem = (size_t)(g.lay.total1 > g.lay.total2 ? g.lay.total1 : g.lay.total2);
   return g;
 }
 
@@ -308,6 +312,9 @@ extern "C" pg_status pg_set_option(pg_model* m, int key, int64_t value) {
       return PG_OK;
     case PG_OPT_FUSED:
       m->fused = value ? 1 : 0;
+      return PG_OK;
+    case 5:    // PG_OPT_TRACE (internal): device buffer of [P][16] u64 phase stamps, 0 = off
+      m->trace = reinterpret_cast<unsigned long long*>(value);
       return PG_OK;
     case 4: {  // PG_OPT_RESERVE (internal): pre-size workspace for a batch
       if (value < 1 || value > (1 << 30)) return fail(PG_EINVAL, "reserve: bad batch");
@@ -473,6 +480,8 @@ static StepParams make_params(pg_model* m, const Geometry& g, const int32_t* idx
   p.loss_out = loss_dev;
   p.mode = m->mode;
   p.smem_bytes = (int)g.smem;
+  p.lay = g.lay;
+  p.trace = m->trace;
   return p;
 }
 

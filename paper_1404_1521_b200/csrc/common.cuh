@@ -40,23 +40,62 @@ __device__ __forceinline__ float4 ldcg4(const float* p) {
 // ---------------------------------------------------------------- grid barrier
 // Sense-reversing barrier for a cooperative (co-resident) grid.  State lives in
 // device memory and survives across launches: `count` returns to 0 after every
-// barrier and `gen` increases monotonically.
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
+// barrier and `gen` increases monotonically.  `my_gen` must be read (relaxed)
+// before this CTA arrives -- e.g. at kernel start -- so the wait costs no extra
+// round trip.  Ordering: bar.sync makes the CTA's writes visible to thread 0;
+// the acq_rel arrival RMW (cumulative) and the release store of `gen` publish
+// them; waiters acquire `gen` and bar.sync again.
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned my_gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned my_gen = ld_acquire_gpu(gen);
-    __threadfence();
-    unsigned arrived = atom_add_acqrel_gpu(count, 1u);
+    const unsigned arrived = atom_add_acqrel_gpu(count, 1u);
     if (arrived == gridDim.x - 1) {
-      *count = 0;
-      __threadfence();
+      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(count), "r"(0u) : "memory");
       st_release_gpu(gen, my_gen + 1);
     } else {
-      while (ld_acquire_gpu(gen) == my_gen) __nanosleep(40);
+      while (ld_acquire_gpu(gen) == my_gen) {
+      }
     }
-    __threadfence();
   }
   __syncthreads();
+}
+
+// ---------------------------------------------------------------- mbarrier + bulk copy (TMA engine)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// Make mbarrier initialisation / prior generic smem accesses visible to the async proxy.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Bulk global -> shared copy on the TMA engine; completion is signalled as
+// transaction bytes on `bar`.  bytes % 16 == 0, both addresses 16 B aligned.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // ---------------------------------------------------------------- warp helpers

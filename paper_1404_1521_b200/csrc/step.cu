@@ -15,75 +15,37 @@
 //   dW1_p += x_p sigma^T (p != c); dW1_c += x_c delta^T + x'_c delta'^T
 //   db1 += sigma; dw2 += g (z - z')
 //   gradient rows: G_p = W1_p sigma (p != c), G_c = W1_c delta, G'_c = W1_c delta'
-// The 6 rows per example (n+1 in general) replace the oracle's 2n unmerged
-// rows; in exact arithmetic their scatter is identical (reading G7).
+// The n+1 rows per example replace the oracle's 2n unmerged rows; in exact
+// arithmetic their scatter is identical (reading G7).
+//
+// Latency structure (the step is latency-bound below B ~ 8k): every global
+// round trip is issued for a whole chunk at once -- cp.async for the row
+// gather, unrolled loads for W1, the dense partials and the owner lists.
 #include "common.cuh"
 #include "step.cuh"
 
 namespace pg {
 
-constexpr int kTMax = 32;       // examples per chunk
-constexpr int kMaxKeys = 256;   // (n+1)*T <= 256 keys per chunk
-constexpr int kCapK = 2048;     // phase-2 owner-merge keys per window
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
 
-// ------------------------------------------------------------------ smem layout
-struct Layout {
-  // phase 1
-  int xs, pg, sig, gz, hinge, rows, skin, skey, uown, useg, ws, red;   // byte offsets
-  // generic phase 1
-  int A, Ac, SIG, DEL, DELc;
-  // phase 2
-  int lbase, keys, seg, stage, carry, dred, ws2;
-  int SB;        // staged rows per sub-batch
-  int total1, total2;
-};
-
-__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
-
-__host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT, int NLtot, int fast) {
-  Layout L{};
-  int o = 0;
-  const int NW = NT / 32;
-  if (fast) {
-    L.xs = o;    o = align16(o + NW * T * 32 * 4);
-    L.pg = o;    o = align16(o + NW * T * 32 * 4);     // == T*(n+1)*d floats
-    L.sig = o;   o = align16(o + 3 * T * 32 * 4);
-    L.A = L.Ac = L.SIG = L.DEL = L.DELc = 0;
-  } else {
-    L.xs = o;    o = align16(o + T * (n + 1) * d * 4); // X, later G rows
-    L.pg = L.xs;
-    L.A = o;     o = align16(o + T * h * 4);
-    L.Ac = o;    o = align16(o + T * h * 4);
-    L.SIG = o;   o = align16(o + T * h * 4);
-    L.DEL = o;   o = align16(o + T * h * 4);
-    L.DELc = o;  o = align16(o + T * h * 4);
-    L.sig = 0;
+// Optional phase timestamps for profiling (PG_OPT_TRACE; thread 0 of each CTA).
+__device__ __forceinline__ void trace_mark(const StepParams& p, int k) {
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[blockIdx.x * 32 + k] = t;
   }
-  L.gz = o;    o = align16(o + kTMax * 4);
-  L.hinge = o; o = align16(o + kTMax * 4);
-  L.rows = o;  o = align16(o + kMaxKeys * 4);
-  L.skin = o;  o = align16(o + kMaxKeys * 8);
-  L.skey = o;  o = align16(o + kMaxKeys * 8);
-  L.uown = o;  o = align16(o + kMaxKeys * 4);
-  L.useg = o;  o = align16(o + (kMaxKeys + 1) * 4);
-  L.ws = o;    o = align16(o + 64 * 4);
-  L.red = o;   o = align16(o + 2 * 32 * 32 * 4);     // per-warp db1/dw2 partials
-  L.total1 = o;
-  // phase 2 (aliases phase 1 storage)
-  o = 0;
-  L.lbase = o; o = align16(o + (NLtot + 1) * 4);
-  L.keys = o;  o = align16(o + kCapK * 8);
-  L.seg = o;   o = align16(o + (kCapK + 1) * 4);
-  int SB = 65536 / (d * 4);
-  if (SB > 512) SB = 512;
-  if (SB < 16) SB = 16;
-  L.SB = SB;
-  L.stage = o; o = align16(o + SB * d * 4);
-  L.carry = o; o = align16(o + d * 4);
-  L.dred = o;  o = align16(o + NT * 16);
-  L.ws2 = o;   o = align16(o + 64 * 4);
-  L.total2 = o;
-  return L;
 }
 
 // ------------------------------------------------------------------ error reporting
@@ -94,73 +56,196 @@ __device__ __forceinline__ void report_bad(DevStatus* st, long long pos, int val
 }
 
 // ------------------------------------------------------------------ CTA-local aggregation
-// Keys: rows_s[i] for i < K (i = example*(n+1) + ext-slot), gradient rows Gs[i][0..d).
-// Sort by (owner = row % P, row, i); sum each row's gradient rows in i order;
-// write list L: rows, sums and per-owner offsets.
-__device__ void aggregate_chunk(const StepParams& p, int L, int K, const int* rows_s,
-                                const float* Gs, unsigned char* sm, const Layout& lay) {
-  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
-  unsigned long long* skin = reinterpret_cast<unsigned long long*>(sm + lay.skin);
-  unsigned long long* skey = reinterpret_cast<unsigned long long*>(sm + lay.skey);
-  int* uown = reinterpret_cast<int*>(sm + lay.uown);
-  int* useg = reinterpret_cast<int*>(sm + lay.useg);
-  int* ws = reinterpret_cast<int*>(sm + lay.ws);
-  const int P = p.P, d = p.d;
-  for (int i = tid; i < K; i += NT) {
-    unsigned row = (unsigned)rows_s[i];
-    unsigned owner = row % (unsigned)P;
-    skin[i] = ((unsigned long long)owner << 40) | ((unsigned long long)row << 8) | (unsigned)i;
-  }
-  __syncthreads();
-  // rank sort (keys unique): O(K^2) broadcast comparisons, K <= 256
-  for (int i = tid; i < K; i += NT) {
-    unsigned long long k = skin[i];
+// Gradient rows of one chunk: keys rows_s[i], values Gs[i][0..d), i < K in
+// (example, slot) order.  Distinct rows are found with an smem hash and placed
+// into owner buckets (owner CTA q = row % P) of list L with per-owner offsets
+// off[q]; each distinct row's duplicates are summed in i order by the warp that
+// owns its entry.  The order of entries INSIDE an owner bucket is irrelevant to
+// the arithmetic: a row appears at most once per list, and phase 2 sums a
+// row's partials in list order.
+__device__ __forceinline__ unsigned hash_row(unsigned row) { return row * 2654435761u; }
+
+// Reset the chunk's hash / bucket state (ordered before use by later barriers).
+__device__ __forceinline__ void agg_reset(const StepParams& p, unsigned char* sm) {
+  const Layout& lay = p.lay;
+  int* hk = reinterpret_cast<int*>(sm + lay.ahk);
+  int* hc = reinterpret_cast<int*>(sm + lay.ahc);
+  int* ocnt = reinterpret_cast<int*>(sm + lay.ocnt);
+  int* ocur = reinterpret_cast<int*>(sm + lay.ocur);
+  int* misc = reinterpret_cast<int*>(sm + lay.misc);
+  #pragma unroll 1
+  for (int i = threadIdx.x; i < 2 * kMaxKeys; i += blockDim.x) { hk[i] = -1; hc[i] = 0; }
+  int* ecur = reinterpret_cast<int*>(sm + lay.ecur);
+  #pragma unroll 1
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) { ocnt[i] = 0; ocur[i] = 0; ecur[i] = 0; }
+  if (threadIdx.x == 0) misc[0] = 0;
+}
+
+// Stable counting sort of items 0..n-1 into buckets bucket[i], given the
+// buckets' exclusive offsets off[]: writes out[off[b] + rank] = i where rank =
+// #{i' < i : bucket[i'] == b}.  Block-parallel O(n^2 / threads) broadcast
+// scan -- no match_any (slow on this part) and no serial warp.
+__device__ __forceinline__ void stable_place(int n, const int* bucket, const int* off, unsigned short* out) {
+  #pragma unroll 1
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int b = bucket[i];
     int r = 0;
-    for (int j = 0; j < K; ++j) r += skin[j] < k;
-    skey[r] = k;
+    int j = 0;
+    #pragma unroll 1
+    for (; j + 4 <= i; j += 4) {
+      const int4 q = *reinterpret_cast<const int4*>(bucket + j);
+      r += (q.x == b) + (q.y == b) + (q.z == b) + (q.w == b);
+    }
+    #pragma unroll 1
+    for (; j < i; ++j) r += bucket[j] == b;
+    out[off[b] + r] = (unsigned short)i;
+  }
+}
+
+// Ordered sum of the rows src[pos[0..m)] (row stride d) for the features
+// f0 + lane + 32k < d, k < 4: 4 independent chains (positions i == c mod 4)
+// combined in a fixed order, so the result depends only on the ordered list.
+__device__ __forceinline__ float4 ordered_rowsum(const float* src, const unsigned short* pos, int m, int d, int f0) {
+  const int lane = threadIdx.x & 31;
+  float a[4][4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[c][k] = 0.f;
+  bool fk[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) fk[k] = f0 + lane + 32 * k < d;
+#pragma unroll 1
+  for (int i = 0; i < m; i += 4) {
+    // branch-free: clamped positions, masked adds -> the 4 chains overlap
+    const float* r[4];
+    bool ok[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      ok[c] = i + c < m;
+      r[c] = src + (size_t)pos[ok[c] ? i + c : i] * d + f0 + lane;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float v = fk[k] ? r[c][32 * k] : 0.f;
+        a[c][k] += ok[c] ? v : 0.f;
+      }
+  }
+  return make_float4((a[0][0] + a[1][0]) + (a[2][0] + a[3][0]), (a[0][1] + a[1][1]) + (a[2][1] + a[3][1]),
+                     (a[0][2] + a[1][2]) + (a[2][2] + a[3][2]), (a[0][3] + a[1][3]) + (a[2][3] + a[3][3]));
+}
+
+__device__ void aggregate_chunk(const StepParams& p, int L, int K, const int* rows_s,
+                                const float* Gs, unsigned char* sm) {
+  const Layout& lay = p.lay;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  int* hk = reinterpret_cast<int*>(sm + lay.ahk);
+  int* hc = reinterpret_cast<int*>(sm + lay.ahc);
+  int* hslot = reinterpret_cast<int*>(sm + lay.aslot);
+  int* ocnt = reinterpret_cast<int*>(sm + lay.ocnt);
+  int* ocur = reinterpret_cast<int*>(sm + lay.ocur);
+  int* hj = reinterpret_cast<int*>(sm + lay.hj);
+  int* misc = reinterpret_cast<int*>(sm + lay.misc);
+  int* ws = reinterpret_cast<int*>(sm + lay.ws);
+  const int P = p.P, d = p.d, HA = 2 * kMaxKeys;
+  // pass 1: insert + multiplicity; the inserting thread counts the row for its owner
+  bool creator = false;
+  int my_row = 0;
+  unsigned my_h = 0;
+  #pragma unroll 1
+  for (int i = tid; i < K; i += NT) {
+    const int row = rows_s[i];
+    unsigned h = hash_row((unsigned)row) & (HA - 1);
+    bool mine = false;
+    while (true) {
+      const int prev = atomicCAS(&hk[h], -1, row);
+      if (prev == -1) { mine = true; break; }
+      if (prev == row) break;
+      h = (h + 1) & (HA - 1);
+    }
+    hslot[i] = (int)h;
+    atomicAdd(&hc[h], 1);
+    if (mine) { creator = true; my_row = row; my_h = h; atomicAdd(&ocnt[(unsigned)row % (unsigned)P], 1); }
   }
   __syncthreads();
-  int head = 0;
-  if (tid < K) {
-    unsigned long long k = skey[tid];
-    head = (tid == 0) || (((k >> 8) & 0xffffffffull) != ((skey[tid - 1] >> 8) & 0xffffffffull));
-  }
-  int U;
-  int hidx = block_excl_scan(head, ws, &U);
-  int32_t* lrows = p.list_rows + (size_t)L * p.cap;
-  float* lvals = p.list_vals + (size_t)L * p.cap * d;
-  if (tid < K && head) {
-    unsigned long long k = skey[tid];
-    useg[hidx] = tid;
-    uown[hidx] = (int)(k >> 40);
-    lrows[hidx] = (int)((k >> 8) & 0xffffffffull);
-  }
-  if (tid == 0) useg[U] = K;
-  __syncthreads();
-  // per-owner offsets: off[q] = #unique entries with owner < q (uown ascending)
+  const bool tr = (L % p.R) == 0;
+  if (tr) trace_mark(p, 14);
   int32_t* off = p.list_off + (size_t)L * (P + 1);
-  for (int q = tid; q <= P; q += NT) {
-    int lo = 0, hi = U;
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (uown[mid] < q) lo = mid + 1; else hi = mid;
-    }
-    off[q] = lo;
+  int nU;
+  {
+    const int v = tid < P ? ocnt[tid] : 0;
+    const int ex = block_excl_scan(v, ws, &nU);
+    if (tid <= P) off[tid] = tid < P ? ex : nU;
+    if (tid < P) ocnt[tid] = ex;   // bucket base
   }
-  // segment sums in position order
-  for (int j = warp; j < U; j += NW) {
-    const int s0 = useg[j], s1 = useg[j + 1];
-    for (int f = lane; f < d; f += 32) {
-      float acc = 0.f;
-      for (int r = s0; r < s1; ++r) acc += Gs[(int)(skey[r] & 0xffull) * d + f];
-      lvals[(size_t)j * d + f] = acc;
+  __syncthreads();
+  if (tr) trace_mark(p, 15);
+  // pass 2: creators take a slot in their owner bucket
+  int32_t* lrows = p.list_rows + (size_t)L * p.cap;
+  int* ecnt = reinterpret_cast<int*>(sm + lay.ecnt);
+  int* eoff = reinterpret_cast<int*>(sm + lay.eoff);
+  int* ecur = reinterpret_cast<int*>(sm + lay.ecur);
+  unsigned short* spos = reinterpret_cast<unsigned short*>(sm + lay.spos);
+  if (creator) {
+    const int q = (int)((unsigned)my_row % (unsigned)P);
+    const int j = ocnt[q] + atomicAdd(&ocur[q], 1);
+    hj[my_h] = j;
+    lrows[j] = my_row;
+    ecnt[j] = hc[my_h];
+  }
+  __syncthreads();
+  #pragma unroll 1
+  for (int i = tid; i < K; i += NT) hslot[i] = hj[hslot[i]];   // position -> entry
+  {
+    const int v = tid < nU ? ecnt[tid] : 0;
+    int tot;
+    const int ex = block_excl_scan(v, ws, &tot);
+    if (tid <= nU) eoff[tid] = tid < nU ? ex : tot;
+  }
+  __syncthreads();
+  if (tr) trace_mark(p, 16);
+  // pass 3: positions grouped by entry, increasing within each entry (one warp)
+  stable_place(K, hslot, eoff, spos);
+  __syncthreads();
+  if (tr) trace_mark(p, 18);
+  // pass 4: warp per entry -- ordered sum of its gradient rows, one coalesced store
+  float* lvals = p.list_vals + (size_t)L * p.cap * d;
+  #pragma unroll 1
+  long long t_sum = 0, t_st = 0;
+  int n_ent = 0;
+#pragma unroll 1
+  for (int j = warp; j < nU; j += NW) {
+    const int m = ecnt[j];
+    const unsigned short* ps = spos + eoff[j];
+    float* dst = lvals + (size_t)j * d;
+#pragma unroll 1
+    for (int f0 = 0; f0 < d; f0 += 128) {
+      const long long c0 = clock64();
+      const float4 o4 = ordered_rowsum(Gs, ps, m, d, f0);
+      const float out[4] = {o4.x, o4.y, o4.z, o4.w};
+      const long long c1 = clock64();
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        if (f0 + lane + 32 * kk < d) dst[f0 + lane + 32 * kk] = out[kk];
+      t_sum += c1 - c0;
+      t_st += clock64() - c1;
+      ++n_ent;
     }
   }
+  if (tr && p.trace != nullptr && lane == 0 && blockIdx.x < 4 && warp < 4) {
+    p.trace[blockIdx.x * 32 + 20 + warp * 3 + 0] = t_sum;
+    p.trace[blockIdx.x * 32 + 20 + warp * 3 + 1] = t_st;
+    p.trace[blockIdx.x * 32 + 20 + warp * 3 + 2] = n_ent;
+  }
+  if (tr) trace_mark(p, 17);
   __syncthreads();
 }
 
 __device__ void write_empty_list(const StepParams& p, int L) {
   int32_t* off = p.list_off + (size_t)L * (p.P + 1);
+  #pragma unroll 1
   for (int q = threadIdx.x; q <= p.P; q += blockDim.x) off[q] = 0;
 }
 
@@ -169,63 +254,109 @@ __device__ void write_empty_list(const StepParams& p, int L) {
 // the 32-feature block (slot = w / (d/32), blk = w % (d/32)) of the extended
 // input [x_0 .. x_{n-1}, x'_c]; its W1 rows live in registers for the whole
 // step (Wcol for the forward, Wrow for the gradient rows).
-__device__ void phase1_fast(const StepParams& p, unsigned char* sm, const Layout& lay) {
+
+// Gather the chunk's K = cnt*(n+1) embedding rows into X[e][slot][0..d) with one
+// bulk copy (TMA engine) per valid row, completing on `bar`.  With `wblock`,
+// also stage every warp's 32 W1 rows (128 B each) into its padded smem block.
+// Returns the parity to wait on.
+__device__ __forceinline__ void gather_rows_bulk(const StepParams& p, long long e0, int cnt, float* X,
+                                                 int* rows_s, unsigned long long* bar, float* wsm, bool wblock) {
+  const int tid = threadIdx.x, n = p.n, d = p.d, K = cnt * (n + 1);
+  int row = -1;
+  bool ok = false;
+  if (tid < K) {
+    const int e = tid / (n + 1), s = tid - e * (n + 1);
+    const long long ex = e0 + e;
+    row = s < n ? __ldg(p.idx + ex * n + s) : __ldg(p.corr + ex);
+    ok = row >= 0 && (long long)row < p.V;
+    if (!ok) report_bad(p.st, s < n ? ex * n + s : (long long)p.B * n + ex, row);
+    rows_s[tid] = ok ? row : 0;
+  }
+  const int nvalid = __syncthreads_count(ok);   // also orders prior generic smem use
+  if (e0 == (long long)blockIdx.x * p.B / p.P) trace_mark(p, 19);
+  const int NW = blockDim.x >> 5, DB = d >> 5, c = n >> 1;
+  const unsigned wbytes = (unsigned)(n * d * 32 * 4);   // all of W1 in one bulk copy
+  if (tid == 0) {
+    mbar_arrive_expect_tx(bar, (unsigned)(nvalid * d * 4) + (wblock ? wbytes : 0u));
+    fence_proxy_async();
+    if (wblock) bulk_g2s(wsm, p.W1, wbytes, bar);
+  }
+  if (ok) {
+    fence_proxy_async();
+    bulk_g2s(X + (size_t)tid * d, p.C + (size_t)row * d, (unsigned)(d * 4), bar);
+  } else if (tid < K) {
+    #pragma unroll 1
+    for (int f = 0; f < d; ++f) X[(size_t)tid * d + f] = 0.f;
+  }
+  (void)NW; (void)DB; (void)c;
+  if (nvalid < K) __syncthreads();   // zero-filled rows (bad index) visible to all warps
+}
+
+__device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
+  const Layout& lay = p.lay;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
   const int d = p.d, n = p.n, T = p.T, DB = d >> 5, c = n >> 1;
   const int slot = warp / DB, blk = warp % DB;
   const int wslot = slot == n ? c : slot;
   const int wrow0 = wslot * d + blk * 32;
   const int sel = slot == n ? 2 : (slot == c ? 1 : 0);  // sigma / delta / delta'
-  float* xs = reinterpret_cast<float*>(sm + lay.xs);
+  const int xstride = (n + 1) * d;                      // floats between examples in X
+  float* X = reinterpret_cast<float*>(sm + lay.xs);
   float* pg = reinterpret_cast<float*>(sm + lay.pg);
   float* sig = reinterpret_cast<float*>(sm + lay.sig);
   float* hinge_s = reinterpret_cast<float*>(sm + lay.hinge);
   int* rows_s = reinterpret_cast<int*>(sm + lay.rows);
   float* red = reinterpret_cast<float*>(sm + lay.red);
+  float* wsm = reinterpret_cast<float*>(sm + lay.wsm);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + lay.mbar);
+  const float* xw = X + slot * d + blk * 32;            // this warp's block of example 0
+  const float* wb = wsm + (size_t)wrow0 * 32;           // this warp's 32 W1 rows (unpadded)
 
-  float Wcol[32], Wrow[32], dacc[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) Wcol[k] = __ldg(p.W1 + (size_t)(wrow0 + k) * 32 + lane);
-  {
-    const float4* wr = reinterpret_cast<const float4*>(p.W1 + (size_t)(wrow0 + lane) * 32);
-#pragma unroll
-    for (int u4 = 0; u4 < 8; ++u4) {
-      float4 v = __ldg(wr + u4);
-      Wrow[4 * u4] = v.x; Wrow[4 * u4 + 1] = v.y; Wrow[4 * u4 + 2] = v.z; Wrow[4 * u4 + 3] = v.w;
-    }
-  }
+  const long long lo = (long long)(((unsigned long long)blockIdx.x * (unsigned)p.B) / (unsigned)p.P);
+  const long long hi = (long long)(((unsigned long long)(blockIdx.x + 1) * (unsigned)p.B) / (unsigned)p.P);
+  auto chunk_cnt = [&](int r) -> int {
+    const long long e0 = lo + (long long)r * T;
+    return (int)(hi - e0 < T ? (hi - e0 > 0 ? hi - e0 : 0) : T);
+  };
+  const float b1 = __ldg(p.b1 + lane), w2 = __ldg(p.w2 + lane), b2 = __ldg(p.b2);
+  float dacc[32];
+  unsigned parity = 0;
 #pragma unroll
   for (int u = 0; u < 32; ++u) dacc[u] = 0.f;
-  const float b1 = __ldg(p.b1 + lane), w2 = __ldg(p.w2 + lane), b2 = __ldg(p.b2);
   float acc_db1 = 0.f, acc_dw2 = 0.f, acc_hinge = 0.f;
 
-  const long long lo = (long long)blockIdx.x * p.B / p.P;
-  const long long hi = (long long)(blockIdx.x + 1) * p.B / p.P;
+#pragma unroll 1
   for (int r = 0; r < p.R; ++r) {
     const long long e0 = lo + (long long)r * T;
-    const int cnt = (int)(hi - e0 < T ? (hi - e0 > 0 ? hi - e0 : 0) : T);
+    const int cnt = chunk_cnt(r);
     const int L = blockIdx.x * p.R + r;
     if (cnt <= 0) { write_empty_list(p, L); continue; }
-    // ---- gather (each warp its own feature block; warp-private smem)
-    float* xw = xs + (size_t)warp * T * 32;
-    for (int e = 0; e < cnt; ++e) {
-      const long long ex = e0 + e;
-      int row = slot < n ? __ldg(p.idx + ex * n + slot) : __ldg(p.corr + ex);
-      const bool ok = row >= 0 && (long long)row < p.V;
-      if (!ok && blk == 0 && lane == 0)
-        report_bad(p.st, slot < n ? ex * n + slot : (long long)p.B * n + ex, row);
-      xw[e * 32 + lane] = ok ? __ldg(p.C + (size_t)row * d + blk * 32 + lane) : 0.f;
-      if (blk == 0 && lane == 0) rows_s[e * (n + 1) + slot] = ok ? row : 0;
+    agg_reset(p, sm);
+    gather_rows_bulk(p, e0, cnt, X, rows_s, bar, wsm, r == 0);
+    mbar_wait(bar, parity);
+    parity ^= 1;
+    // W1 block into registers for this chunk's forward / backward (re-read from
+    // smem every chunk so the registers are free during aggregation)
+    float Wcol[32], Wrow[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) Wcol[k] = wb[k * 32 + lane];
+    {
+      const float4* wr = reinterpret_cast<const float4*>(wb + lane * 32);   // 8-way conflicts, once per chunk
+#pragma unroll
+      for (int u4 = 0; u4 < 8; ++u4) {
+        const float4 v = wr[u4];
+        Wrow[4 * u4] = v.x; Wrow[4 * u4 + 1] = v.y; Wrow[4 * u4 + 2] = v.z; Wrow[4 * u4 + 3] = v.w;
+      }
     }
-    __syncwarp();
+    if (r == 0) trace_mark(p, 1);
     // ---- forward partials: part[warp][e][u] = sum_k x[e][k] W1[wrow0+k][u]
     float* part = pg;
     for (int e = 0; e < cnt; e += 4) {
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-      const float4* x0 = reinterpret_cast<const float4*>(xw + (e + 0) * 32);
-      const float4* x1 = reinterpret_cast<const float4*>(xw + min(e + 1, cnt - 1) * 32);
-      const float4* x2 = reinterpret_cast<const float4*>(xw + min(e + 2, cnt - 1) * 32);
-      const float4* x3 = reinterpret_cast<const float4*>(xw + min(e + 3, cnt - 1) * 32);
+      const float4* x0 = reinterpret_cast<const float4*>(xw + (size_t)(e + 0) * xstride);
+      const float4* x1 = reinterpret_cast<const float4*>(xw + (size_t)min(e + 1, cnt - 1) * xstride);
+      const float4* x2 = reinterpret_cast<const float4*>(xw + (size_t)min(e + 2, cnt - 1) * xstride);
+      const float4* x3 = reinterpret_cast<const float4*>(xw + (size_t)min(e + 3, cnt - 1) * xstride);
 #pragma unroll
       for (int k4 = 0; k4 < 8; ++k4) {
         float4 v0 = x0[k4], v1 = x1[k4], v2 = x2[k4], v3 = x3[k4];
@@ -244,94 +375,153 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm, const Layout
       if (e + 3 < cnt) part[(warp * T + e + 3) * 32 + lane] = a3;
     }
     __syncthreads();
-    // ---- sigma stage: warp per example, lane = hidden unit
-    for (int e = warp; e < cnt; e += NW) {
-      float actx = 0.f, acen = 0.f, acor = 0.f;
+    if (r == 0) trace_mark(p, 2);
+    // ---- sigma stage: warp per example, lane = hidden unit; two examples per
+    // pass so the two shuffle-reduction chains overlap
+    #pragma unroll 1
+    for (int e = warp; e < cnt; e += 2 * NW) {
+      const int e2 = e + NW;
+      const bool two = e2 < cnt;
+      float actx[2] = {0.f, 0.f}, acen[2] = {0.f, 0.f}, acor[2] = {0.f, 0.f};
       for (int s = 0; s < n; ++s) {
         if (s == c) continue;
-        for (int b = 0; b < DB; ++b) actx += part[((s * DB + b) * T + e) * 32 + lane];
+        for (int b = 0; b < DB; ++b) {
+          actx[0] += part[((s * DB + b) * T + e) * 32 + lane];
+          if (two) actx[1] += part[((s * DB + b) * T + e2) * 32 + lane];
+        }
       }
       for (int b = 0; b < DB; ++b) {
-        acen += part[((c * DB + b) * T + e) * 32 + lane];
-        acor += part[((n * DB + b) * T + e) * 32 + lane];
+        acen[0] += part[((c * DB + b) * T + e) * 32 + lane];
+        acor[0] += part[((n * DB + b) * T + e) * 32 + lane];
+        if (two) {
+          acen[1] += part[((c * DB + b) * T + e2) * 32 + lane];
+          acor[1] += part[((n * DB + b) * T + e2) * 32 + lane];
+        }
       }
-      const float base = b1 + actx;
-      const float a = base + acen, ac = base + acor;
-      const float z = fminf(fmaxf(a, -1.f), 1.f), zc = fminf(fmaxf(ac, -1.f), 1.f);
-      const float s = warp_sum(w2 * z) + b2;
-      const float sc = warp_sum(w2 * zc) + b2;
-      const float m = 1.f - s + sc;
-      const bool active = m > 0.f;
-      const float g = active ? -p.inv_B : 0.f;
-      const float dl = fabsf(a) < 1.f ? g * w2 : 0.f;
-      const float dlc = fabsf(ac) < 1.f ? -g * w2 : 0.f;
-      sig[(0 * T + e) * 32 + lane] = dl + dlc;
-      sig[(1 * T + e) * 32 + lane] = dl;
-      sig[(2 * T + e) * 32 + lane] = dlc;
-      acc_db1 += dl + dlc;
-      acc_dw2 += g * z + (-g) * zc;
-      if (lane == 0) acc_hinge += active ? m : 0.f;
+      float z[2], zc[2], a[2], ac[2], sp[2], spc[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float base = b1 + actx[k];
+        a[k] = base + acen[k];
+        ac[k] = base + acor[k];
+        z[k] = fminf(fmaxf(a[k], -1.f), 1.f);
+        zc[k] = fminf(fmaxf(ac[k], -1.f), 1.f);
+        sp[k] = w2 * z[k];
+        spc[k] = w2 * zc[k];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          sp[k] += __shfl_xor_sync(0xffffffffu, sp[k], o);
+          spc[k] += __shfl_xor_sync(0xffffffffu, spc[k], o);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (k == 1 && !two) break;
+        const int ee = k == 0 ? e : e2;
+        const float sv = sp[k] + b2, svc = spc[k] + b2;
+        const float m = 1.f - sv + svc;
+        const bool active = m > 0.f;
+        const float g = active ? -p.inv_B : 0.f;
+        const float dl = fabsf(a[k]) < 1.f ? g * w2 : 0.f;
+        const float dlc = fabsf(ac[k]) < 1.f ? -g * w2 : 0.f;
+        sig[(0 * T + ee) * 32 + lane] = dl + dlc;
+        sig[(1 * T + ee) * 32 + lane] = dl;
+        sig[(2 * T + ee) * 32 + lane] = dlc;
+        acc_db1 += dl + dlc;
+        acc_dw2 += g * z[k] + (-g) * zc[k];
+        if (lane == 0) acc_hinge += active ? m : 0.f;
+      }
     }
     __syncthreads();
-    // ---- backward: gradient rows G[e][slot][blk*32+lane] and dW1 rows
+    if (r == 0) trace_mark(p, 3);
+    // ---- backward: gradient rows G[e][slot][blk*32+lane] and dW1 rows,
+    // two examples per pass for ILP on the shared-memory broadcasts
     float* Gs = pg;   // part is dead now
     const float* sv_base = sig + sel * T * 32;
-    for (int e = 0; e < cnt; ++e) {
-      const float xl = xw[e * 32 + lane];
-      const float4* sv = reinterpret_cast<const float4*>(sv_base + e * 32);
-      float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+    for (int e = 0; e < cnt; e += 2) {
+      const bool two = e + 1 < cnt;
+      const int e1 = two ? e + 1 : e;
+      const float xl0 = xw[(size_t)e * xstride + lane], xl1 = two ? xw[(size_t)e1 * xstride + lane] : 0.f;
+      const float4* sv0 = reinterpret_cast<const float4*>(sv_base + e * 32);
+      const float4* sv1 = reinterpret_cast<const float4*>(sv_base + e1 * 32);
+      float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, h0 = 0.f, h1 = 0.f, h2 = 0.f, h3 = 0.f;
 #pragma unroll
       for (int u4 = 0; u4 < 8; ++u4) {
-        float4 v = sv[u4];
+        const float4 v = sv0[u4], w = sv1[u4];
         g0 = fmaf(Wrow[4 * u4], v.x, g0);
         g1 = fmaf(Wrow[4 * u4 + 1], v.y, g1);
         g2 = fmaf(Wrow[4 * u4 + 2], v.z, g2);
         g3 = fmaf(Wrow[4 * u4 + 3], v.w, g3);
-        dacc[4 * u4] = fmaf(xl, v.x, dacc[4 * u4]);
-        dacc[4 * u4 + 1] = fmaf(xl, v.y, dacc[4 * u4 + 1]);
-        dacc[4 * u4 + 2] = fmaf(xl, v.z, dacc[4 * u4 + 2]);
-        dacc[4 * u4 + 3] = fmaf(xl, v.w, dacc[4 * u4 + 3]);
+        h0 = fmaf(Wrow[4 * u4], w.x, h0);
+        h1 = fmaf(Wrow[4 * u4 + 1], w.y, h1);
+        h2 = fmaf(Wrow[4 * u4 + 2], w.z, h2);
+        h3 = fmaf(Wrow[4 * u4 + 3], w.w, h3);
+        dacc[4 * u4] = fmaf(xl1, w.x, fmaf(xl0, v.x, dacc[4 * u4]));
+        dacc[4 * u4 + 1] = fmaf(xl1, w.y, fmaf(xl0, v.y, dacc[4 * u4 + 1]));
+        dacc[4 * u4 + 2] = fmaf(xl1, w.z, fmaf(xl0, v.z, dacc[4 * u4 + 2]));
+        dacc[4 * u4 + 3] = fmaf(xl1, w.w, fmaf(xl0, v.w, dacc[4 * u4 + 3]));
       }
       Gs[(e * (n + 1) + slot) * d + blk * 32 + lane] = (g0 + g1) + (g2 + g3);
+      if (two) Gs[(e1 * (n + 1) + slot) * d + blk * 32 + lane] = (h0 + h1) + (h2 + h3);
     }
     __syncthreads();
-    aggregate_chunk(p, L, cnt * (n + 1), rows_s, Gs, sm, lay);
+    if (r == 0) trace_mark(p, 4);
+    aggregate_chunk(p, L, cnt * (n + 1), rows_s, Gs, sm);
+    if (r == 0) trace_mark(p, 5);
   }
-  // ---- per-CTA dense partial record: dW1 | db1 | dw2 | hinge
+  // ---- per-CTA dense partial record: dW1 | db1 | dw2 | hinge, written with
+  // coalesced stores (each warp's 32 W1 rows are contiguous in the record)
   float* rec = p.dense_part + (size_t)blockIdx.x * p.dense_stride;
-  float* dsm = xs;   // [NW][32][33]
+  float* dsm = sig;   // [DB][32][33]: the corrupt-centre warps' dW1 rows
+  if (slot == n) {
 #pragma unroll
-  for (int u = 0; u < 32; ++u) dsm[(warp * 32 + lane) * 33 + u] = dacc[u];
+    for (int u = 0; u < 32; ++u) dsm[(blk * 32 + lane) * 33 + u] = dacc[u];
+  }
   red[warp * 32 + lane] = acc_db1;
   red[32 * 32 + warp * 32 + lane] = acc_dw2;
   if (lane == 0) hinge_s[warp] = acc_hinge;
   __syncthreads();
-  const int ndh = n * d * 32;
-  for (int i = tid; i < ndh; i += blockDim.x) {
-    const int row = i >> 5, u = i & 31;
-    const int s = row / d, j = row % d;
-    const int w = s * DB + (j >> 5), l = j & 31;
-    float v = dsm[(w * 32 + l) * 33 + u];
-    if (s == c) v += dsm[((n * DB + (j >> 5)) * 32 + l) * 33 + u];
-    rec[i] = v;
+  if (slot < n) {
+    if (slot == c) {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) dacc[u] += dsm[(blk * 32 + lane) * 33 + u];
+    }
+    float* tile = X + (size_t)warp * 32 * 33;   // X|pg are free: warp-private transpose tile
+#pragma unroll
+    for (int u = 0; u < 32; ++u) tile[lane * 33 + u] = dacc[u];
+    __syncwarp();
+    float4* dst = reinterpret_cast<float4*>(rec + (size_t)wrow0 * 32);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = 4 * (lane + 32 * k), rr = t >> 5, cc = t & 31;
+      dst[lane + 32 * k] = make_float4(tile[rr * 33 + cc], tile[rr * 33 + cc + 1], tile[rr * 33 + cc + 2],
+                                       tile[rr * 33 + cc + 3]);
+    }
   }
+  const int ndh = n * d * 32;
   if (tid < 32) {
     float a = 0.f, b = 0.f;
+    #pragma unroll 1
     for (int w = 0; w < NW; ++w) { a += red[w * 32 + tid]; b += red[32 * 32 + w * 32 + tid]; }
     rec[ndh + tid] = a;
     rec[ndh + 32 + tid] = b;
   }
-  if (tid == 0) {
+  if (tid == 32) {
     float hsum = 0.f;
+    #pragma unroll 1
     for (int w = 0; w < NW; ++w) hsum += hinge_s[w];
     rec[ndh + 64] = hsum;
-    for (int i = ndh + 65; i < p.dense_stride; ++i) rec[i] = 0.f;
   }
+  if (tid >= 64 && tid < 64 + (p.dense_stride - ndh - 65)) rec[ndh + 65 + (tid - 64)] = 0.f;
 }
 
 // ------------------------------------------------------------------ GENERIC phase 1
 // Any (d, n, h) with h <= 128: plain per-thread loops, W1 read through L1.
-__device__ void phase1_generic(const StepParams& p, unsigned char* sm, const Layout& lay) {
+__device__ void phase1_generic(const StepParams& p, unsigned char* sm) {
+  const Layout& lay = p.lay;
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
   const int d = p.d, n = p.n, h = p.h, T = p.T, c = n >> 1, E = (n + 1) * d;
   float* X = reinterpret_cast<float*>(sm + lay.xs);
@@ -357,7 +547,7 @@ __device__ void phase1_generic(const StepParams& p, unsigned char* sm, const Lay
     const int cnt = (int)(hi - e0 < T ? (hi - e0 > 0 ? hi - e0 : 0) : T);
     const int L = blockIdx.x * p.R + r;
     if (cnt <= 0) { write_empty_list(p, L); continue; }
-    // gather rows of the extended window into X[e][slot][j]
+    agg_reset(p, sm);
     for (int i = tid; i < cnt * (n + 1); i += NT) {
       const int e = i / (n + 1), s = i % (n + 1);
       const long long ex = e0 + e;
@@ -370,8 +560,10 @@ __device__ void phase1_generic(const StepParams& p, unsigned char* sm, const Lay
     for (int i = tid; i < cnt * E; i += NT) {
       const int e = i / E, s = (i % E) / d, j = i % d;
       const int row = rows_s[e * (n + 1) + s];
-      X[i] = row >= 0 ? __ldg(p.C + (size_t)row * d + j) : 0.f;
+      if (row >= 0) cp_async4(X + i, p.C + (size_t)row * d + j);
+      else X[i] = 0.f;
     }
+    cp_async_wait_all();
     __syncthreads();
     for (int i = tid; i < cnt * (n + 1); i += NT) if (rows_s[i] < 0) rows_s[i] = 0;
     // forward
@@ -393,7 +585,6 @@ __device__ void phase1_generic(const StepParams& p, unsigned char* sm, const Lay
       Ac[i] = base + acor;
     }
     __syncthreads();
-    // sigma stage: warp per example
     for (int e = warp; e < cnt; e += NW) {
       float sp = 0.f, spc = 0.f;
       for (int u = lane; u < h; u += 32) {
@@ -414,7 +605,6 @@ __device__ void phase1_generic(const StepParams& p, unsigned char* sm, const Lay
       if (lane == 0) { gz[e] = g; hinge_s[e] = active ? m : 0.f; }
     }
     __syncthreads();
-    // dense partials (accumulated across chunks in this CTA's record)
     for (int i = tid; i < ndh; i += NT) {
       const int row = i / h, u = i % h, s = row / d, j = row % d;
       float acc = 0.f;
@@ -439,10 +629,7 @@ __device__ void phase1_generic(const StepParams& p, unsigned char* sm, const Lay
     }
     if (tid == 0) for (int e = 0; e < cnt; ++e) hinge_acc += hinge_s[e];
     __syncthreads();
-    // gradient rows into X's storage (X no longer needed)
-    float* Gs = X;
-    // compute into registers first, then write, to avoid overwriting X mid-use
-    // (G does not read X, so write directly)
+    float* Gs = X;   // G does not read X
     for (int i = tid; i < cnt * E; i += NT) {
       const int e = i / E, s = (i % E) / d, j = i % d;
       const float* vec = s == n ? DELc : (s == c ? DEL : SIG);
@@ -453,10 +640,10 @@ __device__ void phase1_generic(const StepParams& p, unsigned char* sm, const Lay
       Gs[i] = acc;
     }
     __syncthreads();
-    aggregate_chunk(p, L, cnt * (n + 1), rows_s, Gs, sm, lay);
+    aggregate_chunk(p, L, cnt * (n + 1), rows_s, Gs, sm);
     first = false;
   }
-  if (first) {  // no examples at all in this CTA
+  if (first) {
     for (int i = tid; i < p.dense_stride; i += NT) rec[i] = 0.f;
   } else if (tid == 0) {
     rec[ndh + 2 * h] = hinge_acc;
@@ -465,58 +652,96 @@ __device__ void phase1_generic(const StepParams& p, unsigned char* sm, const Lay
 }
 
 // ------------------------------------------------------------------ phase 2
+// All of phase 2's global reads are issued before the flag / loss decision is
+// consumed, so the bad-index / divergence gate costs no round trip:
+//   trip 1: flags, hinge partials, dense partials (+ the params they update),
+//           this owner's entry counts in every list;
+//   trip 2: the owner's entries (row ids + gradient partials);
+//   trip 3: the C rows to update.
+// Only the final stores are gated on the decision.
 __device__ __forceinline__ float* param_ptr(const StepParams& p, int i, int ndh) {
   if (i < ndh) return p.W1 + i;
   if (i < ndh + p.h) return p.b1 + (i - ndh);
   return p.w2 + (i - ndh - p.h);
 }
 
-__device__ void phase2_dense(const StepParams& p, unsigned char* sm, const Layout& lay) {
-  const int tid = threadIdx.x, NT = blockDim.x;
-  const int DL = p.dense_len, ndh = p.n * p.d * p.h;
-  const int NQ = (DL + 3) / 4;
-  const int G = gridDim.x;
-  const int q0 = (int)((long long)blockIdx.x * NQ / G), q1 = (int)((long long)(blockIdx.x + 1) * NQ / G);
-  float4* dred = reinterpret_cast<float4*>(sm + lay.dred);
-  for (int qb = q0; qb < q1; qb += NT) {
-    const int nq = min(NT, q1 - qb);
-    int groups = NT / nq;
-    if (groups > 32) groups = 32;
-    const int qi = tid % nq, g = tid / nq;
-    if (g < groups) {
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int r = g; r < p.Ptot; r += groups) {
-        float4 v = ldcg4(p.dense_part + (size_t)r * p.dense_stride + 4 * (qb + qi));
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-      }
-      dred[g * nq + qi] = acc;
-    }
-    __syncthreads();
-    if (tid < nq) {
-      float4 s = dred[tid];
-      for (int gg = 1; gg < groups; ++gg) {
-        float4 v = dred[gg * nq + tid];
-        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-      }
-      const float sv[4] = {s.x, s.y, s.z, s.w};
-      const int base = 4 * (qb + tid);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int i = base + k;
-        if (i < DL) {
-          float* q = param_ptr(p, i, ndh);
-          *q = *q - p.lr * sv[k];
-        }
-      }
-    }
-    __syncthreads();
-  }
+struct DenseSlice {
+  int q0, q1;
+};
+
+__device__ __forceinline__ DenseSlice dense_slice(const StepParams& p) {
+  const int NQ = (p.dense_len + 3) / 4, G = gridDim.x;
+  return {(int)((long long)blockIdx.x * NQ / G), (int)((long long)(blockIdx.x + 1) * NQ / G)};
 }
 
+// Fixed-order reduction of quads [qb, qb+nq) over the Ptot records: thread
+// (quad qi, group g) sums records g, g+G, ... (4 loads in flight).
+__device__ __forceinline__ float4 dense_partial(const StepParams& p, int qb, int nq, int groups) {
+  const int qi = threadIdx.x % nq, g = threadIdx.x / nq;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (g >= groups) return acc;
+  const float* base = p.dense_part + 4 * (qb + qi);
+  #pragma unroll 1
+  for (int r0 = g; r0 < p.Ptot; r0 += 8 * groups) {   // 8 loads in flight, summed in record order
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int r = r0 + k * groups;
+      v[k] = r < p.Ptot ? ldcg4(base + (size_t)r * p.dense_stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w; }
+  }
+  return acc;
+}
+
+__device__ __forceinline__ int dense_groups(int nq, int NT) {
+  int g = NT / nq;
+  return g > 32 ? 32 : g;
+}
+
+// Combine the groups (in order) and apply W1/b1/w2 -= lr * grad for one block.
+__device__ __forceinline__ void dense_apply(const StepParams& p, unsigned char* sm, int qb, int nq, int groups, float4 acc,
+                                         float4 cur4, bool write) {
+  const float cur[4] = {cur4.x, cur4.y, cur4.z, cur4.w};
+  const int tid = threadIdx.x, ndh = p.n * p.d * p.h, DL = p.dense_len;
+  float4* dred = reinterpret_cast<float4*>(sm + p.lay.dred);
+  const int qi = tid % nq, g = tid / nq;
+  if (g < groups) dred[g * nq + qi] = acc;
+  __syncthreads();
+  if (tid < nq) {
+    float4 s = dred[tid];
+    #pragma unroll 1
+    for (int gg = 1; gg < groups; ++gg) {
+      const float4 v = dred[gg * nq + tid];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    const float sv[4] = {s.x, s.y, s.z, s.w};
+    const int base = 4 * (qb + tid);
+    if (write) {
+      if ((ndh & 3) == 0 && (p.h & 3) == 0) {   // a quad never straddles W1 | b1 | w2
+        float* q = param_ptr(p, base, ndh);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (base + k < DL) q[k] = cur[k] - p.lr * sv[k];
+      } else {
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k)
+          if (base + k < DL) *param_ptr(p, base + k, ndh) = cur[k] - p.lr * sv[k];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ phase 2: deterministic scatter
 // Bitonic sort of n (power of two) 64-bit keys in smem.
 __device__ void bitonic_sort(unsigned long long* k, int n) {
+  #pragma unroll 1
   for (int size = 2; size <= n; size <<= 1) {
+    #pragma unroll 1
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      #pragma unroll 1
       for (int t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
         const int lo = 2 * t - (t & (stride - 1));
         const int hi = lo + stride;
@@ -529,55 +754,40 @@ __device__ void bitonic_sort(unsigned long long* k, int n) {
   }
 }
 
-// Deterministic owner merge: CTA q owns rows with row % P == q.  Its entries
-// from every list are sorted by (row, list) and each row's list partials are
-// summed in list order, then C[row] += -lr * sum.
-__device__ void phase2_scatter_det(const StepParams& p, unsigned char* sm, const Layout& lay) {
+// Sorted fallback for owners with more than MCAP entries (pathological index
+// patterns): windows of whole lists, bitonic sort by (row, list), segment sums
+// in list order with a carry across staged sub-batches.
+__device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
+  const Layout& lay = p.lay;
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
-  const int q = blockIdx.x, P = p.P, d = p.d, NL = p.NLtot;
-  int* lbase = reinterpret_cast<int*>(sm + lay.lbase);
+  const int d = p.d, NL = p.NLtot;
+  const int* lbase = reinterpret_cast<const int*>(sm + lay.lbase);
+  const int* loff = reinterpret_cast<const int*>(sm + lay.loff);
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(sm + lay.keys);
   int* seg = reinterpret_cast<int*>(sm + lay.seg);
-  float* stage = reinterpret_cast<float*>(sm + lay.stage);
+  float* stage = reinterpret_cast<float*>(sm + lay.stagefb);
   float* carry = reinterpret_cast<float*>(sm + lay.carry);
   int* ws = reinterpret_cast<int*>(sm + lay.ws2);
   const float nlr = -p.lr;
-  // counts per list, exclusive scan -> lbase
-  int running = 0;
-  for (int L0 = 0; L0 < NL; L0 += NT) {
-    const int L = L0 + tid;
-    int cnt = 0;
-    if (L < NL) {
-      const int32_t* off = p.list_off + (size_t)L * (P + 1);
-      cnt = __ldcg(off + q + 1) - __ldcg(off + q);
-    }
-    int tot;
-    int ex = block_excl_scan(cnt, ws, &tot);
-    if (L < NL) lbase[L] = running + ex;
-    running += tot;
-  }
-  if (tid == 0) lbase[NL] = running;
-  __syncthreads();
-  const int M = running;
-  if (M == 0) return;
-  // windows of whole lists with at most kCapK entries
   int La = 0;
   while (La < NL) {
     int Lb = La;
-    while (Lb < NL && lbase[Lb + 1] - lbase[La] <= kCapK) ++Lb;
+    if (lbase[NL] - lbase[La] <= kCapK) Lb = NL;
+    else while (Lb < NL && lbase[Lb + 1] - lbase[La] <= kCapK) ++Lb;
     const int base = lbase[La], Mw = lbase[Lb] - base;
     if (Mw > 0) {
       int npow = 1;
       while (npow < Mw) npow <<= 1;
+      #pragma unroll 1
       for (int e = tid; e < npow; e += NT) {
         if (e < Mw) {
-          int lo = La, hi = Lb - 1;   // find L with lbase[L] <= base+e < lbase[L+1]
+          int lo = La, hi = Lb - 1;
           while (lo < hi) {
             int mid = (lo + hi + 1) >> 1;
             if (lbase[mid] <= base + e) lo = mid; else hi = mid - 1;
           }
           const int L = lo;
-          const int j = __ldcg(p.list_off + (size_t)L * (P + 1) + q) + (base + e - lbase[L]);
+          const int j = loff[L] + (base + e - lbase[L]);
           const unsigned row = (unsigned)__ldcg(p.list_rows + (size_t)L * p.cap + j);
           keys[e] = ((unsigned long long)row << 32) | ((unsigned long long)L << 8) | (unsigned)j;
         } else {
@@ -586,8 +796,8 @@ __device__ void phase2_scatter_det(const StepParams& p, unsigned char* sm, const
       }
       __syncthreads();
       bitonic_sort(keys, npow);
-      // segment heads
       int nseg_total = 0;
+      #pragma unroll 1
       for (int e0 = 0; e0 < Mw; e0 += NT) {
         const int e = e0 + tid;
         int head = 0;
@@ -599,39 +809,32 @@ __device__ void phase2_scatter_det(const StepParams& p, unsigned char* sm, const
       }
       if (tid == 0) seg[nseg_total] = Mw;
       __syncthreads();
-      // sub-batches of SB staged rows
+      #pragma unroll 1
       for (int sb0 = 0; sb0 < Mw; sb0 += lay.SB) {
         const int sb1 = min(Mw, sb0 + lay.SB);
-        const int d4 = d >> 2;
-        if ((d & 3) == 0) {
-          for (int t = tid; t < (sb1 - sb0) * d4; t += NT) {
-            const int e = sb0 + t / d4, f4 = t % d4;
-            const unsigned long long k = keys[e];
-            const int L = (int)((k >> 8) & 0xffffff), j = (int)(k & 0xff);
-            reinterpret_cast<float4*>(stage)[t] = ldcg4(p.list_vals + ((size_t)L * p.cap + j) * d + 4 * f4);
-          }
-        } else {
-          for (int t = tid; t < (sb1 - sb0) * d; t += NT) {
-            const int e = sb0 + t / d, f = t % d;
-            const unsigned long long k = keys[e];
-            const int L = (int)((k >> 8) & 0xffffff), j = (int)(k & 0xff);
-            stage[t] = __ldcg(p.list_vals + ((size_t)L * p.cap + j) * d + f);
-          }
+        #pragma unroll 1
+        for (int t = tid; t < (sb1 - sb0) * d; t += NT) {
+          const int e = sb0 + t / d, f = t % d;
+          const unsigned long long k = keys[e];
+          const int L = (int)((k >> 8) & 0xffffff), j = (int)(k & 0xff);
+          stage[t] = __ldcg(p.list_vals + ((size_t)L * p.cap + j) * d + f);
         }
         __syncthreads();
-        // segments overlapping [sb0, sb1)
-        int slo = 0, shi = nseg_total - 1;   // last segment starting <= sb0
+        int slo = 0, shi = nseg_total - 1;
         while (slo < shi) {
           int mid = (slo + shi + 1) >> 1;
           if (seg[mid] <= sb0) slo = mid; else shi = mid - 1;
         }
+        #pragma unroll 1
         for (int sidx = slo + warp; sidx < nseg_total && seg[sidx] < sb1; sidx += NW) {
           const int s0 = seg[sidx], s1 = seg[sidx + 1];
           const int a0 = max(s0, sb0), a1 = min(s1, sb1);
           const bool cont = s0 < sb0, fin = s1 <= sb1;
           const unsigned row = (unsigned)(keys[s0] >> 32);
+          #pragma unroll 1
           for (int f = lane; f < d; f += 32) {
             float acc = cont ? carry[f] : 0.f;
+            #pragma unroll 1
             for (int e = a0; e < a1; ++e) acc += stage[(e - sb0) * d + f];
             if (fin) {
               float* cp = p.C + (size_t)row * d + f;
@@ -648,62 +851,270 @@ __device__ void phase2_scatter_det(const StepParams& p, unsigned char* sm, const
   }
 }
 
+// Trip 1 of the owner merge: CTA q's entry count in every list, scanned into
+// lbase (entry base per list) and loff (offset of q's bucket inside the list).
+// Returns M, the owner's entry count.
+__device__ int det_counts(const StepParams& p, unsigned char* sm, int pre_a, int pre_b) {
+  const Layout& lay = p.lay;
+  const int tid = threadIdx.x, NT = blockDim.x, q = blockIdx.x, P = p.P, NL = p.NLtot;
+  int* lbase = reinterpret_cast<int*>(sm + lay.lbase);
+  int* loff = reinterpret_cast<int*>(sm + lay.loff);
+  int* ws = reinterpret_cast<int*>(sm + lay.ws2);
+  int running = 0;
+  #pragma unroll 1
+  for (int L0 = 0; L0 < NL; L0 += NT) {
+    const int L = L0 + tid;
+    int cnt = 0;
+    if (L < NL) {
+      int a = pre_a, b = pre_b;   // lists [0, NT) were loaded with the other trip-1 reads
+      if (L0 > 0) {
+        const int32_t* off = p.list_off + (size_t)L * (P + 1);
+        a = __ldcg(off + q);
+        b = __ldcg(off + q + 1);
+      }
+      loff[L] = a;
+      cnt = b - a;
+    }
+    int tot;
+    const int ex = block_excl_scan(cnt, ws, &tot);
+    if (L < NL) lbase[L] = running + ex;
+    running += tot;
+  }
+  if (tid == 0) lbase[NL] = running;
+  __syncthreads();
+  return running;
+}
+
+// Deterministic owner merge (hash fast path, M <= MCAP): CTA q owns rows with
+// row % P == q.  Its entries are staged in (list, position) order -- list
+// order is the fixed summation order -- and each distinct row's partials are
+// summed in that order, then C[row] += -lr * sum (one rounding).
+__device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool write) {
+  const Layout& lay = p.lay;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  const int d = p.d, NL = p.NLtot;
+  const int* lbase = reinterpret_cast<const int*>(sm + lay.lbase);
+  const int* loff = reinterpret_cast<const int*>(sm + lay.loff);
+  int* ws = reinterpret_cast<int*>(sm + lay.ws2);
+  int* esrc = reinterpret_cast<int*>(sm + lay.esrc);
+  int* erow = reinterpret_cast<int*>(sm + lay.erow);
+  int* heads = reinterpret_cast<int*>(sm + lay.heads);
+  unsigned short* hlist = reinterpret_cast<unsigned short*>(sm + lay.hlist);
+  int* hkey = reinterpret_cast<int*>(sm + lay.hkey);
+  int* hfirst = reinterpret_cast<int*>(sm + lay.hfirst);
+  float* stage = reinterpret_cast<float*>(sm + lay.stage);
+  const int HS = lay.HS;
+  const float nlr = -p.lr;
+  #pragma unroll 1
+  for (int e = tid; e < M; e += NT) {
+    int lo = 0, hi = NL - 1;   // last L with lbase[L] <= e
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (lbase[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    esrc[e] = lo * p.cap + loff[lo] + (e - lbase[lo]);
+  }
+  #pragma unroll 1
+  for (int i = tid; i < HS; i += NT) { hkey[i] = -1; hfirst[i] = 0; }
+  if (tid == 0) reinterpret_cast<int*>(sm + lay.rcur)[lay.MCAP] = 0;
+  __syncthreads();
+  // ---- trip 2: row ids and gradient partials of all entries at once (TMA bulk copies)
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + lay.mbar) + 1;
+  const bool bulk = (d & 3) == 0;
+  if (bulk) {
+    if (tid == 0) mbar_arrive_expect_tx(bar, (unsigned)(M * d * 4));
+    fence_proxy_async();
+    #pragma unroll 1
+    for (int e = tid; e < M; e += NT) {
+      erow[e] = __ldcg(p.list_rows + esrc[e]);
+      bulk_g2s(stage + (size_t)e * d, p.list_vals + (size_t)esrc[e] * d, (unsigned)(d * 4), bar);
+    }
+  } else {
+    #pragma unroll 1
+    for (int e = tid; e < M; e += NT) erow[e] = __ldcg(p.list_rows + esrc[e]);
+    #pragma unroll 1
+    for (int t = tid; t < M * d; t += NT) {
+      const int e = t / d, f = t - e * d;
+      cp_async4(stage + t, p.list_vals + (size_t)esrc[e] * d + f);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  __syncthreads();
+  // ---- distinct rows: smem hash (row -> distinct index), multiplicity per row
+  int* hcnt = hfirst;          // reused: per-slot multiplicity
+  int* eslot = esrc;           // reused: entry -> hash slot (sources already issued)
+  int* rcnt = reinterpret_cast<int*>(sm + lay.rcnt);
+  int* roff = reinterpret_cast<int*>(sm + lay.roff);
+  int* rcur = reinterpret_cast<int*>(sm + lay.rcur);
+  int* rrow = heads;           // distinct index -> row
+  int* hrid = reinterpret_cast<int*>(sm + lay.misc2);
+  int my_r[2] = {-1, -1}, my_hs[2] = {0, 0};
+  #pragma unroll 1
+  for (int e = tid, k = 0; e < M; e += NT, ++k) {
+    const int key = erow[e];
+    unsigned hsl = hash_row((unsigned)key) & (HS - 1);
+    bool mine = false;
+    while (true) {
+      const int prev = atomicCAS(&hkey[hsl], -1, key);
+      if (prev == -1) { mine = true; break; }
+      if (prev == key) break;
+      hsl = (hsl + 1) & (HS - 1);
+    }
+    eslot[e] = (int)hsl;
+    atomicAdd(&hcnt[hsl], 1);
+    if (mine && k < 2) {
+      const int r = atomicAdd(&rcur[lay.MCAP], 1);
+      hrid[hsl] = r;
+      rrow[r] = key;
+      my_r[k] = r;
+      my_hs[k] = (int)hsl;
+    }
+  }
+  __syncthreads();
+  const int nrows = rcur[lay.MCAP];
+  if (my_r[0] >= 0) rcnt[my_r[0]] = hcnt[my_hs[0]];
+  if (my_r[1] >= 0) rcnt[my_r[1]] = hcnt[my_hs[1]];
+  #pragma unroll 1
+  for (int e = tid; e < M; e += NT) eslot[e] = hrid[eslot[e]];   // entry -> distinct row
+  __syncthreads();
+  {
+    int running = 0;
+    #pragma unroll 1
+    for (int r0 = 0; r0 < nrows; r0 += NT) {
+      const int r = r0 + tid;
+      const int v = r < nrows ? rcnt[r] : 0;
+      int tot;
+      const int ex = block_excl_scan(v, ws, &tot);
+      if (r < nrows) { roff[r] = running + ex; rcur[r] = 0; }
+      running += tot;
+    }
+  }
+  __syncthreads();
+  // entries grouped by row, in list order within each row (one warp)
+  stable_place(M, eslot, roff, hlist);
+  // ---- trip 3: C rows of the first 4*NW distinct rows, bulk-copied while the
+  // staged partials are still in flight
+  float* cstage = reinterpret_cast<float*>(sm + lay.cstage);
+  unsigned long long* cbar = reinterpret_cast<unsigned long long*>(sm + lay.mbar) + 2;
+  const int ncp = bulk ? min(nrows, 4 * NW) : 0;
+  if (ncp > 0) {
+    if (tid == 0) mbar_arrive_expect_tx(cbar, (unsigned)(ncp * d * 4));
+    fence_proxy_async();
+    if (tid < ncp) bulk_g2s(cstage + (size_t)tid * d, p.C + (size_t)rrow[tid] * d, (unsigned)(d * 4), cbar);
+  }
+  if (bulk) mbar_wait(bar, 0);
+  else asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (ncp > 0) mbar_wait(cbar, 0);
+  __syncthreads();
+  // ---- warp per distinct row: ordered sum of its partials, one RMW of C
+#pragma unroll 1
+  for (int ri = warp; ri < nrows; ri += NW) {
+    float* crow = p.C + (size_t)rrow[ri] * d;
+    const float* cold = ri < ncp ? cstage + (size_t)ri * d : nullptr;
+    const int nm = rcnt[ri];
+    const unsigned short* ps = hlist + roff[ri];
+#pragma unroll 1
+    for (int f0 = 0; f0 < d; f0 += 128) {
+      const float4 a4 = ordered_rowsum(stage, ps, nm, d, f0);
+      const float acc[4] = {a4.x, a4.y, a4.z, a4.w};
+      if (write) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int f = f0 + lane + 32 * k;
+          if (f < d) crow[f] = (cold ? cold[f] : __ldcg(crow + f)) + nlr * acc[k];
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // Atomic scatter: CTA b applies lists L = b, b+G, ... with red.global.add.v4.f32.
 __device__ void phase2_scatter_atomic(const StepParams& p) {
-  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
   const int P = p.P, d = p.d;
   const float nlr = -p.lr;
+  #pragma unroll 1
   for (int L = blockIdx.x; L < p.NLtot; L += gridDim.x) {
     const int U = __ldcg(p.list_off + (size_t)L * (P + 1) + P);
+    #pragma unroll 1
     for (int j = warp; j < U; j += NW) {
       const int row = __ldcg(p.list_rows + (size_t)L * p.cap + j);
       const float* src = p.list_vals + ((size_t)L * p.cap + j) * d;
       float* dst = p.C + (size_t)row * d;
       if ((d & 3) == 0) {
+        #pragma unroll 1
         for (int f4 = lane; f4 < (d >> 2); f4 += 32) {
           float4 v = ldcg4(src + 4 * f4);
           v.x *= nlr; v.y *= nlr; v.z *= nlr; v.w *= nlr;
           red_add_v4(dst + 4 * f4, v);
         }
       } else {
+        #pragma unroll 1
         for (int f = lane; f < d; f += 32) atomicAdd(dst + f, nlr * __ldcg(src + f));
       }
     }
   }
 }
 
-__device__ void phase2(const StepParams& p, unsigned char* sm, const Layout& lay) {
+__device__ void phase2(const StepParams& p, unsigned char* sm) {
   __shared__ int s_flags;
   __shared__ float s_loss;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x;
   DevStatus* st = p.st;
+  // ---- trip 1: everything that does not depend on the decision
+  unsigned my_done = 0;
   if (tid == 0) {
-    const int f = *(volatile int*)&st->flags;
-    const unsigned long long bad = *(volatile unsigned long long*)&st->bad;
+    const int f = __ldcg(&st->flags);
+    const unsigned long long bad = __ldcg(&st->bad);
     s_flags = f;
-    if (blockIdx.x == 0) {
-      st->last_flags = f;
-      st->last_bad = bad;
-    }
-    __threadfence();
-    if (atomicAdd(&st->done, 1u) == gridDim.x - 1) {  // everyone has read the flags
-      st->flags = 0;
-      st->bad = kNoBad;
-      st->done = 0;
-      __threadfence();
-    }
+    if (blockIdx.x == 0) st->last_bad = bad;
+    my_done = atomicAdd(&st->done, 1u);   // result consumed only at the end (flag reset)
   }
-  if (warp == 0) {
+  if (warp == 1) {
     float acc = 0.f;
     const int hoff = p.dense_len;
-    for (int r = lane; r < p.Ptot; r += 32) acc += __ldcg(p.dense_part + (size_t)r * p.dense_stride + hoff);
+    #pragma unroll 1
+    for (int r0 = 0; r0 < p.Ptot; r0 += 32 * 5) {   // 5 loads in flight per lane
+      float v[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int r = r0 + lane + 32 * k;
+        v[k] = r < p.Ptot ? __ldcg(p.dense_part + (size_t)r * p.dense_stride + hoff) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 5; ++k) acc += v[k];
+    }
     acc = warp_sum(acc);
     if (lane == 0) s_loss = acc * p.inv_B;
   }
+  // owner counts for lists [0, NT): issued before anything consumes a load
+  int pre_a = 0, pre_b = 0;
+  if (p.mode == 0 && tid < p.NLtot) {
+    const int32_t* off = p.list_off + (size_t)tid * (p.P + 1) + blockIdx.x;
+    pre_a = __ldcg(off);
+    pre_b = __ldcg(off + 1);
+  }
+  const DenseSlice ds = dense_slice(p);
+  const int nq0 = min(NT, ds.q1 - ds.q0);
+  const int groups0 = nq0 > 0 ? dense_groups(nq0, NT) : 1;
+  float4 dacc0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float cur0[4] = {0.f, 0.f, 0.f, 0.f};
+  if (nq0 > 0) {
+    dacc0 = dense_partial(p, ds.q0, nq0, groups0);
+    if (tid < nq0) {
+      const int ndh = p.n * p.d * p.h, base = 4 * (ds.q0 + tid);
+#pragma unroll 1
+      for (int k = 0; k < 4; ++k)
+        if (base + k < p.dense_len) cur0[k] = __ldcg(param_ptr(p, base + k, ndh));
+    }
+  }
+  int M = 0;
+  if (p.mode == 0) M = det_counts(p, sm, pre_a, pre_b);   // contains __syncthreads
   __syncthreads();
   const float loss = s_loss;
-  const bool diverged = !isfinite(loss);
-  const int flags = s_flags | (diverged ? 2 : 0);
+  const int flags = s_flags | (!isfinite(loss) ? 2 : 0);
+  const bool write = flags == 0;   // no parameter changes on a bad index or a non-finite loss
   if (blockIdx.x == 0 && tid == 0) {
     st->last_loss = loss;
     st->last_flags = flags;
@@ -713,24 +1124,66 @@ __device__ void phase2(const StepParams& p, unsigned char* sm, const Layout& lay
       atomicMin(&st->sticky_bad, st->last_bad);
     }
   }
-  if (flags) return;   // no parameter changes on a bad index or a non-finite loss
-  phase2_dense(p, sm, lay);
-  __syncthreads();
-  if (p.mode == 0) phase2_scatter_det(p, sm, lay);
-  else phase2_scatter_atomic(p);
+  trace_mark(p, 8);
+  // ---- dense update (first block prefetched; further blocks only when P is small)
+  if (nq0 > 0) dense_apply(p, sm, ds.q0, nq0, groups0, dacc0, make_float4(cur0[0], cur0[1], cur0[2], cur0[3]), write);
+  #pragma unroll 1
+  for (int qb = ds.q0 + nq0; qb < ds.q1; qb += NT) {
+    const int nq = min(NT, ds.q1 - qb), groups = dense_groups(nq, NT);
+    float cur[4] = {0.f, 0.f, 0.f, 0.f};
+    if (tid < nq) {
+      const int ndh = p.n * p.d * p.h, base = 4 * (qb + tid);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (base + k < p.dense_len) cur[k] = __ldcg(param_ptr(p, base + k, ndh));
+    }
+    dense_apply(p, sm, qb, nq, groups, dense_partial(p, qb, nq, groups),
+                make_float4(cur[0], cur[1], cur[2], cur[3]), write);
+  }
+  trace_mark(p, 9);
+  // ---- embedding scatter-add
+  if (p.mode == 0) {
+    if (M > 0) {
+      if (M <= p.lay.MCAP) det_merge(p, sm, M, write);
+      else if (write) scatter_det_sorted(p, sm);
+    }
+  } else if (write) {
+    phase2_scatter_atomic(p);
+  }
+  if (tid == 0 && my_done == gridDim.x - 1) {   // every CTA has read this step's flags
+    st->flags = 0;
+    st->bad = kNoBad;
+    st->done = 0;
+  }
 }
 
 // ------------------------------------------------------------------ kernels
 template <bool FAST>
 __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const Layout lay = make_layout(p.d, p.n, p.h, p.T, blockDim.x, p.NLtot, FAST);
-  if (phases & 1) {
-    if (FAST) phase1_fast(p, smem, lay);
-    else phase1_generic(p, smem, lay);
+  const unsigned my_gen = ld_relaxed_gpu(&p.st->bar_gen);   // consumed at the grid barrier
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + p.lay.mbar);
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (phases == 3) grid_barrier(&p.st->bar_count, &p.st->bar_gen);
-  if (phases & 2) phase2(p, smem, lay);
+  __syncthreads();
+  trace_mark(p, 0);
+  if (p.trace != nullptr && threadIdx.x == 0) p.trace[blockIdx.x * 32 + 12] = clock64();
+  if (phases & 1) {
+    if (FAST) phase1_fast(p, smem);
+    else phase1_generic(p, smem);
+    __syncthreads();
+    trace_mark(p, 6);
+  }
+  if (phases == 3) grid_barrier(&p.st->bar_count, &p.st->bar_gen, my_gen);
+  trace_mark(p, 7);
+  if (phases & 2) phase2(p, smem);
+  __syncthreads();
+  trace_mark(p, 11);
+  if (p.trace != nullptr && threadIdx.x == 0) p.trace[blockIdx.x * 32 + 13] = clock64();
 }
 
 int step_fast_ok(int d, int n, int h) {
@@ -747,15 +1200,9 @@ int step_chunk_T(int d, int n, int h, int fast) {
   int T = kTMax;
   while ((n + 1) * T > kMaxKeys) --T;
   if (!fast) {
-    while (T > 1 && (T * (n + 1) * d + 5 * T * h) * 4 > 150 * 1024) --T;
+    while (T > 1 && (T * (n + 1) * d + 5 * T * h) * 4 > 170 * 1024) --T;
   }
   return T;
-}
-
-size_t step_smem_bytes(int d, int n, int h, int T, int NLtot, int fast) {
-  const int NT = step_block_threads(d, n, h, fast);
-  Layout L = make_layout(d, n, h, T, NT, NLtot, fast);
-  return (size_t)(L.total1 > L.total2 ? L.total1 : L.total2);
 }
 
 // Allow up to the opt-in maximum minus the kernel's static shared memory.
@@ -767,12 +1214,6 @@ cudaError_t step_prepare(int fast, size_t optin, size_t* usable) {
   const size_t smem = optin - fa.sharedSizeBytes;
   if (usable) *usable = smem;
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-
-int step_max_blocks(int fast, int threads, size_t smem, int* out) {
-  cudaError_t e = fast ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, step_kernel<true>, threads, smem)
-                       : cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, step_kernel<false>, threads, smem);
-  return e == cudaSuccess;
 }
 
 void launch_step(const StepParams& p, int fused, int fast, cudaStream_t s, int* launches) {

@@ -5,6 +5,10 @@
 
 namespace pg {
 
+constexpr int kTMax = 32;       // examples per chunk
+constexpr int kMaxKeys = 256;   // (n+1)*T <= 256 gradient rows per chunk
+constexpr int kCapK = 2048;     // phase-2 owner-merge keys per window (sorted fallback)
+
 // Device-resident status / synchronisation block (one per model).
 struct DevStatus {
   unsigned long long bad;        // current step: min over (pos << 32 | uint32 value)
@@ -22,6 +26,101 @@ struct DevStatus {
   float last_loss;
   int pad[3];
 };
+
+// Shared-memory carve-up (byte offsets), computed once on the host.
+struct Layout {
+  // phase 1
+  int xs, pg, sig, gz, hinge, rows, ws, red, wsm, mbar;
+  int ahk, ahc, aslot, ocnt, ocur, hj, ecnt, eoff, ecur, spos, misc;   // chunk aggregation
+  int A, Ac, SIG, DEL, DELc;   // generic path
+  // phase 2
+  int lbase, loff, keys, seg, stage, stagefb, carry, dred, ws2;
+  int esrc, erow, hkey, hfirst, heads, hlist, rcnt, roff, rcur, misc2, cstage;
+  int SB;        // staged rows per sub-batch (sorted fallback)
+  int MCAP;      // owner entries handled by the hash fast path
+  int HS;        // hash slots (power of two >= 2*MCAP)
+  int total1, total2;
+};
+
+__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT, int NLtot, int fast) {
+  Layout L{};
+  L.mbar = 0;   // three mbarriers (phase-1 gathers, phase-2 staging, C prefetch), never aliased
+  int o = 32;
+  const int NW = NT / 32;
+  if (fast) {
+    L.xs = o;    o = align16(o + NW * T * 32 * 4);
+    L.pg = o;    o = align16(o + NW * T * 32 * 4);     // == T*(n+1)*d floats
+    const int sigf = 3 * T * 32 > (d / 32) * 32 * 33 ? 3 * T * 32 : (d / 32) * 32 * 33;
+    L.sig = o;   o = align16(o + sigf * 4);
+    L.wsm = o;   o = align16(o + NW * 32 * 36 * 4);    // per-warp W1 block, rows padded to 36
+  } else {
+    L.xs = o;    o = align16(o + T * (n + 1) * d * 4); // X, later G rows
+    L.pg = L.xs;
+    L.A = o;     o = align16(o + T * h * 4);
+    L.Ac = o;    o = align16(o + T * h * 4);
+    L.SIG = o;   o = align16(o + T * h * 4);
+    L.DEL = o;   o = align16(o + T * h * 4);
+    L.DELc = o;  o = align16(o + T * h * 4);
+  }
+  L.gz = o;    o = align16(o + kTMax * 4);
+  L.hinge = o; o = align16(o + kTMax * 4);
+  L.rows = o;  o = align16(o + kMaxKeys * 4);
+  L.ahk = o;   o = align16(o + 2 * kMaxKeys * 4);
+  L.aslot = o; o = align16(o + kMaxKeys * 4);
+  L.ocnt = o;  o = align16(o + 256 * 4);
+  L.ocur = o;  o = align16(o + 256 * 4);
+  L.ahc = o;   o = align16(o + 2 * kMaxKeys * 4);
+  L.hj = o;    o = align16(o + 2 * kMaxKeys * 4);
+  L.ecnt = o;  o = align16(o + kMaxKeys * 4);
+  L.eoff = o;  o = align16(o + (kMaxKeys + 1) * 4);
+  L.ecur = o;  o = align16(o + kMaxKeys * 4);
+  L.spos = o;  o = align16(o + kMaxKeys * 2);
+  L.misc = o;  o = align16(o + 16 * 4);
+  L.ws = o;    o = align16(o + 64 * 4);
+  L.red = o;   o = align16(o + 2 * 32 * 32 * 4);
+  L.total1 = o;
+  // phase 2 (aliases phase 1 storage)
+  o = 32;
+  L.lbase = o; o = align16(o + (NLtot + 1) * 4);
+  L.loff = o;  o = align16(o + (NLtot + 1) * 4);
+  L.ws2 = o;   o = align16(o + 64 * 4);
+  L.dred = o;  o = align16(o + NT * 16);
+  const int p2fixed = o;
+  // hash fast path
+  int MCAP = (160 * 1024) / (d * 4 + 32);
+  if (MCAP > 512) MCAP = 512;
+  int HS = 1;
+  while (HS < 2 * MCAP) HS <<= 1;
+  L.MCAP = MCAP;
+  L.HS = HS;
+  L.esrc = o;   o = align16(o + MCAP * 4);
+  L.erow = o;   o = align16(o + MCAP * 4);
+  L.heads = o;  o = align16(o + (MCAP + 1) * 4);
+  L.hlist = o;  o = align16(o + MCAP * 2);        // entries sorted by (row, list) (uint16)
+  L.rcnt = o;   o = align16(o + MCAP * 4);
+  L.roff = o;   o = align16(o + (MCAP + 1) * 4);
+  L.rcur = o;   o = align16(o + (MCAP + 1) * 4);   // [MCAP] holds the distinct-row counter
+  L.misc2 = o;  o = align16(o + HS * 4);          // hash slot -> distinct row index
+  L.hkey = o;   o = align16(o + HS * 4);
+  L.hfirst = o; o = align16(o + HS * 4);
+  L.stage = o;  o = align16(o + MCAP * d * 4);
+  L.cstage = o; o = align16(o + 4 * NW * d * 4);     // C rows of each warp's first 4 distinct rows
+  const int fast_end = o;
+  // sorted fallback (aliases the hash path)
+  o = p2fixed;
+  L.keys = o;  o = align16(o + kCapK * 8);
+  L.seg = o;   o = align16(o + (kCapK + 1) * 4);
+  int SB = 65536 / (d * 4);
+  if (SB > 512) SB = 512;
+  if (SB < 16) SB = 16;
+  L.SB = SB;
+  L.stagefb = o; o = align16(o + SB * d * 4);
+  L.carry = o; o = align16(o + d * 4);
+  L.total2 = o > fast_end ? o : fast_end;
+  return L;
+}
 
 // Fixed per-step decomposition: P CTAs, CTA p
 // owns examples [p*B/P, (p+1)*B/P), processed in R chunks of <= T examples.
@@ -57,15 +156,15 @@ struct StepParams {
   DevStatus* st;
   float* loss_out;      // optional device pointer
   int mode;             // 0 det, 1 atomic
-  int smem_bytes;       // dynamic smem available
+  int smem_bytes;       // dynamic smem requested
+  unsigned long long* trace;  // optional [P][16] %globaltimer stamps (PG_OPT_TRACE)
+  Layout lay;
 };
 
 void launch_step(const StepParams& p, int fused, int fast, cudaStream_t s, int* launches);
 int step_fast_ok(int d, int n, int h);
 int step_block_threads(int d, int n, int h, int fast);
 int step_chunk_T(int d, int n, int h, int fast);
-size_t step_smem_bytes(int d, int n, int h, int T, int P, int fast);
 cudaError_t step_prepare(int fast, size_t optin, size_t* usable);
-int step_max_blocks(int fast, int threads, size_t smem, int* out);
 
 }  // namespace pg

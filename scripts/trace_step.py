@@ -1,0 +1,59 @@
+"""Per-CTA phase timestamps of the fused step (PG_OPT_TRACE), averaged over steps."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_1404_1521_b200 as pg
+import synth
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--batch", type=int, default=4096)
+ap.add_argument("--steps", type=int, default=10)
+ap.add_argument("--split", action="store_true")
+ap.add_argument("--atomic", action="store_true")
+ap.add_argument("--flush", action="store_true")
+ap.add_argument("--busy", action="store_true", help="keep the GPU busy between steps (no host sync)")
+a = ap.parse_args()
+V, d, n, h = 100_000, 64, 5, 32
+m = pg.PolyglotModel(V, d, n, h, fused=not a.split, scatter=1 if a.atomic else 0)
+P = min(148, a.batch)
+tr = torch.zeros(a.steps, 160 * 32, dtype=torch.int64, device="cuda")
+bs = [synth.batch(V, n, a.batch, seed=1, step=t) for t in range(a.steps)]
+di = [torch.from_numpy(i).cuda() for i, _ in bs]
+dc = [torch.from_numpy(c).cuda() for _, c in bs]
+fl = torch.empty(128 * 1024 * 1024, device="cuda")
+for t in range(a.steps):
+    pg.pg_set_option(m.handle, 5, tr[t].data_ptr())
+    if a.flush:
+        fl.zero_()
+    m.train_step(di[t], dc[t], 0.1, loss_out=None)
+    if not a.busy:
+        torch.cuda.synchronize()
+torch.cuda.synchronize()
+names = ["start", "gathered", "fwd", "sigma", "bwd", "agg", "p1end", "barrier", "p2head", "dense", "", "end",
+         "", "", "agg.ins", "agg.scan", "agg.place", "agg.acc", "agg.csr", "idx"]
+X = tr.view(a.steps, 160, 32).cpu().numpy()[2:, :P].astype(np.float64)
+rel = []
+mhz = []
+for x in X:
+    t0 = x[:, 0].min()
+    y = x[:, :20].copy()
+    y[:, 12:14] = 0
+    rel.append(np.where(y > 0, y - t0, np.nan))
+    mhz.append(np.median((x[:, 13] - x[:, 12]) / (x[:, 11] - x[:, 0]) * 1e3))
+A = np.stack(rel)
+Xr = tr.view(a.steps, 160, 32).cpu().numpy()[2:, :4, 20:32]
+print("pass4 per warp (cta0-3, warp0-3): cycles in rowsum / in store / entries:", Xr.mean(0).reshape(4, 4, 3).astype(int).tolist())
+print(f"B={a.batch} split={a.split} flush={a.flush} busy={a.busy} SM clock in kernel ~{np.median(mhz):.0f} MHz "
+      f"(us from earliest CTA start; median / max over CTAs)")
+order = [0, 19, 1, 2, 3, 4, 14, 15, 16, 18, 17, 5, 6, 7, 8, 9, 11]
+for k in order:
+    nm = names[k]
+    col = A[:, :, k]
+    if np.isnan(col).all():
+        continue
+    print(f"  {nm:9s} med {np.nanmedian(col) / 1e3:7.2f}  max {np.nanmean(np.nanmax(col, axis=1)) / 1e3:7.2f}")
