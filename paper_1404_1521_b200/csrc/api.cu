@@ -266,7 +266,7 @@ extern "C" pg_status pg_init(pg_model** out, int64_t vocab, int32_t dim, int32_t
   z.bad = z.last_bad = z.sticky_bad = z.score_bad = kNoBad;
   cudaMemcpy(m->st, &z, sizeof z, cudaMemcpyHostToDevice);
   cudaError_t e2 = step_prepare(m->fast, prop.sharedMemPerBlockOptin, &m->smem_max);
-  if (e2 == cudaSuccess) e2 = scatter_prepare(2048);
+  if (e2 == cudaSuccess) e2 = scatter_prepare(1024);
   if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e2 == cudaSuccess) e2 = cudaDeviceSynchronize();
   if (e2 != cudaSuccess) return bail(fail(PG_ECUDA, "pg_init: %s", cudaGetErrorString(e2)));
@@ -560,7 +560,7 @@ static pg_status scatter_common(float* W, int64_t rows, int32_t cols, const floa
     g_sc_ws[dev] = nullptr;
     CU(cudaMalloc(&g_sc_ws[dev], pl.total_bytes));
     g_sc_cap[dev] = pl.total_bytes;
-    CU(scatter_prepare(2048));   // the largest digit table any plan uses
+    CU(scatter_prepare(1024));   // the largest digit table any plan uses
   }
   int l = 0;
   CU(scatter_launch(pl, g_sc_ws[dev], W, rows, cols, Y, I, n, mode, s, &l));

@@ -3,13 +3,16 @@
 // and for each row, each cell in the row is added in parallel")
 // as two sm_100a pipelines behind pg_scatter_add:
 //
-// DET (bit-reproducible): stable LSD radix sort of (I[k], k) in 2 passes of
-//   <= 11-bit digits (histogram kernel + one onesweep kernel per pass with
-//   decoupled look-back), then a segmented reduction over fixed chunks of S
-//   sorted entries: every segment sums its Y rows in k order; segments that
-//   cross chunk boundaries leave per-chunk partials that a fix-up kernel
-//   combines in chunk order with a fixed-shape tree.  One read-modify-write of
-//   W per (row, chunk) -- in practice one per unique row.
+// DET (bit-reproducible): stable LSD radix sort of (I[k], k) in passes of
+//   <= 10-bit digits -- per pass an upsweep (per-tile digit counts), a
+//   two-launch scan of the digit-major count matrix and a downsweep (stable
+//   in-tile ranks by warp ballots, staged in smem, coalesced write-out) --
+//   then a segmented reduction over fixed chunks of kChunk sorted entries:
+//   every segment sums its Y rows in k order (Y rows stream through a cp.async
+//   ring); segments that cross chunk boundaries leave per-chunk partials that a
+//   fix-up kernel combines in chunk order with a fixed-shape tree.  Every row
+//   receives exactly ONE vector reduction of its fixed-order total, so the
+//   result does not depend on timing.
 // ATOMIC: validation pass, then red.global.add.v4.f32 per 16 B of each Y row
 //   (FTZ), no ordering guarantee.
 #include "common.cuh"
@@ -17,60 +20,136 @@
 
 namespace pg {
 
-constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 keys per tile
+constexpr int kSortThreads = 1024;
+constexpr int kSortItems = 8;
+constexpr int kSortTile = kSortThreads * kSortItems;   // 8192 keys per tile
+constexpr int kMaxDigitBits = 10;
 constexpr int kChunk = 256;                             // sorted entries per reduce chunk
-constexpr unsigned kFlagA = 1u << 30, kFlagP = 2u << 30, kCountMask = (1u << 30) - 1;
+constexpr int kScanBlocks = 128;
+constexpr int kRing = 16;                               // Y rows staged per reduce warp
+constexpr int kRWarps = 8;                              // warps per reduce block
 
-// ------------------------------------------------------------------ histogram + validation
-__global__ void __launch_bounds__(512) sc_hist(const int32_t* __restrict__ I, int64_t n, int64_t rows,
-                                               int passes, int bits, int* __restrict__ hist,
-                                               ScatterStatus* st) {
-  extern __shared__ int sh[];
-  const int bins = 1 << bits;
-  for (int i = threadIdx.x; i < passes * bins; i += blockDim.x) sh[i] = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-    const int64_t e = base + threadIdx.x;
-    const bool valid = e < n;
-    int key = valid ? __ldg(I + e) : 0;
-    if (valid && (key < 0 || (int64_t)key >= rows)) {
-      atomicMin(&st->bad, ((unsigned long long)e << 32) | (unsigned)key);
-      atomicOr(&st->flag, 1);
-      key = 0;
-    }
-    for (int p = 0; p < passes; ++p) {
-      const int dig = valid ? ((unsigned)key >> (p * bits)) & (bins - 1) : bins;
-      const unsigned peers = __match_any_sync(0xffffffffu, dig);
-      if (valid && lane == __ffs(peers) - 1) atomicAdd(&sh[p * bins + dig], __popc(peers));
-    }
+// ------------------------------------------------------------------ radix sort
+// Lanes of the warp whose `dig` (bits wide) equals this lane's, among `valid`
+// lanes: one ballot per digit bit (match.any is microcoded and slow here).
+__device__ __forceinline__ unsigned warp_match(unsigned dig, int bits, bool valid) {
+  unsigned peers = __ballot_sync(0xffffffffu, valid);
+  for (int b = 0; b < bits; ++b) {
+    const bool bit = (dig >> b) & 1u;
+    const unsigned bb = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? bb : ~bb;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < passes * bins; i += blockDim.x)
-    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+  return peers;
 }
 
-// ------------------------------------------------------------------ onesweep pass
-// dynamic smem: whist[NW][bins] + tpref[bins] + ws[32]
-__global__ void __launch_bounds__(kSortThreads) sc_onesweep(
-    const int32_t* __restrict__ kin, const int32_t* __restrict__ vin, int32_t* __restrict__ kout,
-    int32_t* __restrict__ vout, int64_t n, int shift, int bits, const int* __restrict__ hist,
-    unsigned* lookback, unsigned* tile_ctr, const ScatterStatus* st) {
-  extern __shared__ int sh[];
-  __shared__ int s_tile;
+// counts[d * ntiles + tile] = #keys of the tile with digit d (per-warp smem
+// histograms, one aggregated atomic per distinct digit per warp step).  With
+// rows > 0 (first pass) the indices are also validated.
+__global__ void __launch_bounds__(kSortThreads) sc_upsweep(const int32_t* __restrict__ kin, int64_t n, int shift,
+                                                           int bits, int64_t rows, int* __restrict__ counts,
+                                                           ScatterStatus* st) {
+  extern __shared__ int sh[];   // [NW][bins]
   const int bins = 1 << bits, NW = kSortThreads / 32;
-  int* whist = sh;                    // [NW][bins]
-  int* tpref = sh + NW * bins;        // [bins]
-  int* ws = tpref + bins;             // [32]
+  const int tile = blockIdx.x, ntiles = gridDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < NW * bins; i += kSortThreads) sh[i] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)tile * kSortTile + (int64_t)warp * 32 * kSortItems;
+  const unsigned lt = (1u << lane) - 1u;
+  int* wh = sh + warp * bins;
+  int key[kSortItems];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int64_t e = base + j * 32 + lane;
+    key[j] = e < n ? __ldg(kin + e) : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int64_t e = base + j * 32 + lane;
+    const bool valid = e < n;
+    int k = key[j];
+    if (valid && rows > 0 && (k < 0 || (int64_t)k >= rows)) {
+      atomicMin(&st->bad, ((unsigned long long)e << 32) | (unsigned)k);
+      atomicOr(&st->flag, 1);
+      k = 0;
+    }
+    const unsigned dig = ((unsigned)k >> shift) & (bins - 1);
+    const unsigned peers = warp_match(dig, bits, valid);
+    if (valid && (peers & lt) == 0) atomicAdd(&wh[dig], __popc(peers));
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < bins; d += kSortThreads) {
+    int c = 0;
+    for (int w = 0; w < NW; ++w) c += sh[w * bins + d];
+    counts[(size_t)d * ntiles + tile] = c;
+  }
+}
+
+// Exclusive scan of the digit-major count matrix (m ints) in two launches:
+// block b reduces segment [b*m/NB, (b+1)*m/NB) (coalesced), then rescans it
+// with the sum of the earlier segments added.
+__global__ void __launch_bounds__(256) sc_scan_reduce(const int* __restrict__ a, int m, int* __restrict__ bsum,
+                                                      const ScatterStatus* st) {
+  __shared__ int ws[32];
+  if (*(volatile const int*)&st->flag) return;
+  const int s0 = (int)((long long)blockIdx.x * m / gridDim.x);
+  const int s1 = (int)((long long)(blockIdx.x + 1) * m / gridDim.x);
+  int sum = 0;
+#pragma unroll 4
+  for (int i = s0 + threadIdx.x; i < s1; i += 256) sum += __ldg(a + i);
+  int tot;
+  block_excl_scan(sum, ws, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(256) sc_scan_apply(int* __restrict__ a, int m, const int* __restrict__ bsum,
+                                                     const ScatterStatus* st) {
+  __shared__ int ws[32];
+  if (*(volatile const int*)&st->flag) return;
+  const int s0 = (int)((long long)blockIdx.x * m / gridDim.x);
+  const int s1 = (int)((long long)(blockIdx.x + 1) * m / gridDim.x);
+  const int pre = (int)threadIdx.x < (int)blockIdx.x ? __ldg(bsum + threadIdx.x) : 0;
+  int carry;
+  block_excl_scan(pre, ws, &carry);   // sum of the earlier segments
+  for (int r0 = s0; r0 < s1; r0 += 256 * 4) {
+    int v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = r0 + threadIdx.x * 4 + k;
+      v[k] = i < s1 ? a[i] : 0;
+    }
+    int rt;
+    int ex = carry + block_excl_scan(v[0] + v[1] + v[2] + v[3], ws, &rt);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = r0 + threadIdx.x * 4 + k;
+      if (i < s1) a[i] = ex;
+      ex += v[k];
+    }
+    carry += rt;
+  }
+}
+
+// Stable in-tile ranking by warp ballots, then the tile is staged in digit
+// order in smem and written out with coalesced runs.
+// dynamic smem: whist[NW][bins] + tpref[bins] + tstart[bins] + skey[tile] + sval[tile]
+__global__ void __launch_bounds__(kSortThreads) sc_downsweep(
+    const int32_t* __restrict__ kin, const int32_t* __restrict__ vin, int32_t* __restrict__ kout,
+    int32_t* __restrict__ vout, int64_t n, int shift, int bits, const int* __restrict__ offs,
+    const ScatterStatus* st) {
+  extern __shared__ int sh[];
+  __shared__ int ws[32];
+  const int bins = 1 << bits, NW = kSortThreads / 32;
+  int* whist = sh;
+  int* tpref = whist + NW * bins;
+  int* tstart = tpref + bins;
+  int* skey = tstart + bins;
+  int* sval = skey + kSortTile;
   if (*(volatile const int*)&st->flag) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = (int)atomicAdd(tile_ctr, 1u);
+  const int tile = blockIdx.x, ntiles = gridDim.x;
   for (int i = tid; i < NW * bins; i += kSortThreads) whist[i] = 0;
+  for (int d = tid; d < bins; d += kSortThreads) tpref[d] = __ldg(offs + (size_t)d * ntiles + tile);
   __syncthreads();
-  const int tile = s_tile;
   const int64_t base = (int64_t)tile * kSortTile + (int64_t)warp * 32 * kSortItems;
   const unsigned lt = (1u << lane) - 1u;
   int keys[kSortItems], vals[kSortItems], lrank[kSortItems];
@@ -85,60 +164,41 @@ __global__ void __launch_bounds__(kSortThreads) sc_onesweep(
   for (int j = 0; j < kSortItems; ++j) {
     const int64_t e = base + j * 32 + lane;
     const bool valid = e < n;
-    const int dig = valid ? ((unsigned)keys[j] >> shift) & (bins - 1) : bins;
-    const unsigned peers = __match_any_sync(0xffffffffu, dig);
+    const unsigned dig = valid ? ((unsigned)keys[j] >> shift) & (bins - 1) : 0u;
+    const unsigned peers = warp_match(dig, bits, valid);
     const int before = valid ? whist[warp * bins + dig] : 0;
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) whist[warp * bins + dig] = before + __popc(peers);
+    if (valid && (peers & lt) == 0) whist[warp * bins + dig] = before + __popc(peers);
     __syncwarp();
     lrank[j] = before + __popc(peers & lt);
   }
   __syncthreads();
-  // global exclusive prefix of the digit histogram (each tile recomputes it)
-  const int per = (bins + kSortThreads - 1) / kSortThreads;   // <= 8
-  {
-    int loc[8];
-    int sum = 0;
-    for (int k = 0; k < per; ++k) {
-      const int dg = tid * per + k;
-      loc[k] = dg < bins ? __ldg(hist + dg) : 0;
-      sum += loc[k];
-    }
-    int tot;
-    int ex = block_excl_scan(sum, ws, &tot);
-    for (int k = 0; k < per; ++k) {
-      const int dg = tid * per + k;
-      if (dg < bins) tpref[dg] = ex;
-      ex += loc[k];
+  // per digit: exclusive over warps (warp order == position order) and the tile
+  // total; then the in-tile digit starts (exclusive over digits)
+  const int per = (bins + kSortThreads - 1) / kSortThreads;   // <= 1 (bins <= 1024)
+  int tot_d[4];
+  int sum = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    tot_d[k] = 0;
+    const int dg = tid * per + k;
+    if (k < per && dg < bins) {
+      int run = 0;
+      for (int w = 0; w < NW; ++w) {
+        const int t = whist[w * bins + dg];
+        whist[w * bins + dg] = run;
+        run += t;
+      }
+      tot_d[k] = run;
+      sum += run;
     }
   }
-  __syncthreads();
-  // per digit: exclusive over warps, tile count, decoupled look-back
-  for (int dg = tid; dg < bins; dg += kSortThreads) {
-    int run = 0;
-    for (int w = 0; w < NW; ++w) {
-      const int t = whist[w * bins + dg];
-      whist[w * bins + dg] = run;
-      run += t;
-    }
-    unsigned* slot = lookback + (size_t)tile * bins + dg;
-    if (tile == 0) {
-      st_release_gpu(slot, kFlagP | (unsigned)run);
-    } else {
-      st_release_gpu(slot, kFlagA | (unsigned)run);
-      unsigned excl = 0;
-      int t = tile - 1;
-      while (true) {
-        const unsigned v = ld_acquire_gpu(lookback + (size_t)t * bins + dg);
-        const unsigned f = v & ~kCountMask;
-        if (f == 0) continue;            // predecessor not published yet
-        excl += v & kCountMask;
-        if (f == kFlagP) break;
-        --t;
-      }
-      st_release_gpu(slot, kFlagP | (excl + (unsigned)run));
-      tpref[dg] += (int)excl;
-    }
+  int all;
+  int ex = block_excl_scan(sum, ws, &all);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int dg = tid * per + k;
+    if (k < per && dg < bins) { tstart[dg] = ex; ex += tot_d[k]; }
   }
   __syncthreads();
 #pragma unroll
@@ -146,42 +206,35 @@ __global__ void __launch_bounds__(kSortThreads) sc_onesweep(
     const int64_t e = base + j * 32 + lane;
     if (e < n) {
       const int dig = ((unsigned)keys[j] >> shift) & (bins - 1);
-      const int pos = tpref[dig] + whist[warp * bins + dig] + lrank[j];
-      kout[pos] = keys[j];
-      vout[pos] = vals[j];
+      const int loc = tstart[dig] + whist[warp * bins + dig] + lrank[j];
+      skey[loc] = keys[j];
+      sval[loc] = vals[j];
     }
+  }
+  __syncthreads();
+  const int64_t rem = n - (int64_t)tile * kSortTile;
+  const int cnt = (int)(rem < kSortTile ? rem : kSortTile);
+#pragma unroll 4
+  for (int i = tid; i < cnt; i += kSortThreads) {
+    const int k = skey[i];
+    const int dig = ((unsigned)k >> shift) & (bins - 1);
+    const int pos = tpref[dig] + (i - tstart[dig]);
+    kout[pos] = k;
+    vout[pos] = sval[i];
   }
 }
 
 // ------------------------------------------------------------------ segmented reduction
-// Warp per chunk of kChunk sorted entries.  VEC floats per lane per row step.
 template <int VEC>
 __device__ __forceinline__ void load_row(const float* __restrict__ src, int cols, int lane, float* v) {
   if (VEC == 4) {
-    float4 t = __ldg(reinterpret_cast<const float4*>(src) + lane);
+    float4 t = __ldcg(reinterpret_cast<const float4*>(src) + lane);
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
   } else if (VEC == 2) {
-    float2 t = __ldg(reinterpret_cast<const float2*>(src) + lane);
+    float2 t = __ldcg(reinterpret_cast<const float2*>(src) + lane);
     v[0] = t.x; v[1] = t.y;
   } else {
-    v[0] = lane < cols ? __ldg(src + lane) : 0.f;
-  }
-}
-
-template <int VEC>
-__device__ __forceinline__ void store_rmw(float* dst, int cols, int lane, const float* acc) {
-  if (VEC == 4) {
-    float4* p = reinterpret_cast<float4*>(dst) + lane;
-    float4 t = __ldcg(p);
-    t.x += acc[0]; t.y += acc[1]; t.z += acc[2]; t.w += acc[3];
-    *p = t;
-  } else if (VEC == 2) {
-    float2* p = reinterpret_cast<float2*>(dst) + lane;
-    float2 t = __ldcg(p);
-    t.x += acc[0]; t.y += acc[1];
-    *p = t;
-  } else if (lane < cols) {
-    dst[lane] = __ldcg(dst + lane) + acc[0];
+    v[0] = lane < cols ? __ldcg(src + lane) : 0.f;
   }
 }
 
@@ -196,120 +249,212 @@ __device__ __forceinline__ void store_plain(float* dst, int cols, int lane, cons
   }
 }
 
-// cols == 32*VEC for VEC in {2, 4}; VEC == 1 handles cols <= 32.
+// One vector reduction of a finished row sum onto W.  In DET mode every row
+// receives exactly one such add per call (its fixed-order total), so
+// W_old + total does not depend on timing; the vector red flushes subnormals.
 template <int VEC>
-__global__ void __launch_bounds__(256) sc_reduce(const int32_t* __restrict__ skeys,
-                                                 const int32_t* __restrict__ svals,
-                                                 const float* __restrict__ Y, float* W, int cols,
-                                                 int64_t n, float* carry, const ScatterStatus* st) {
-  if (*(volatile const int*)&st->flag) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t nchunks = (n + kChunk - 1) / kChunk;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  constexpr int U = 8;   // rows in flight per warp
-  for (int64_t c = gw; c < nchunks; c += nwarps) {
-    const int64_t c0 = c * kChunk, c1 = min(n, c0 + kChunk);
-    const bool first_cont = c0 > 0 && __ldg(skeys + c0) == __ldg(skeys + c0 - 1);
-    const bool last_cont = c1 < n && __ldg(skeys + c1 - 1) == __ldg(skeys + c1);
-    float acc[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
-    bool seg_started_before = first_cont;
-    for (int64_t b0 = c0; b0 < c1; b0 += 32) {
-      const int64_t e = b0 + lane;
-      const int mykey = e < c1 ? __ldg(skeys + e) : -1;
-      const int mypos = e < c1 ? __ldg(svals + e) : 0;
-      const int nxt = (e + 1 < c1) ? __ldg(skeys + e + 1) : -2;   // -2: chunk end
-      const int cnt = (int)(c1 - b0 < 32 ? c1 - b0 : 32);
-      for (int j0 = 0; j0 < cnt; j0 += U) {
-        float r[U][VEC];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int j = j0 + u;
-          const int pos = __shfl_sync(0xffffffffu, mypos, j & 31);
-          if (j < cnt) load_row<VEC>(Y + (size_t)pos * cols, cols, lane, r[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int j = j0 + u;
-          const int key = __shfl_sync(0xffffffffu, mykey, j & 31);
-          const int next = __shfl_sync(0xffffffffu, nxt, j & 31);
-          if (j < cnt) {
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[v] += r[u][v];
-            if (next != key) {   // segment ends at this entry
-              const bool at_chunk_end = (next == -2);
-              const bool continues = at_chunk_end && last_cont;
-              if (!seg_started_before && !continues) {
-                store_rmw<VEC>(W + (size_t)key * cols, cols, lane, acc);
-              } else if (seg_started_before) {
-                store_plain<VEC>(carry + (size_t)(2 * c) * cols, cols, lane, acc);
-              } else {
-                store_plain<VEC>(carry + (size_t)(2 * c + 1) * cols, cols, lane, acc);
-              }
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
-              seg_started_before = false;
-            }
-          }
-        }
-      }
-    }
+__device__ __forceinline__ void red_row(float* dst, int cols, int lane, const float* acc) {
+  if (VEC == 4) {
+    red_add_v4(dst + 4 * lane, make_float4(acc[0], acc[1], acc[2], acc[3]));
+  } else if (VEC == 2) {   // pair lanes: 16 lanes x 16 B vector reductions
+    const float a0 = __shfl_down_sync(0xffffffffu, acc[0], 1);
+    const float a1 = __shfl_down_sync(0xffffffffu, acc[1], 1);
+    if ((lane & 1) == 0) red_add_v4(dst + 2 * lane, make_float4(acc[0], acc[1], a0, a1));
+  } else if (lane < cols) {
+    atomicAdd(dst + lane, acc[0]);
   }
 }
 
-// Chains of chunk partials for segments that cross chunk boundaries.
+// Warp per chunk of kChunk sorted entries.  The chunk's (key, pos) pairs are
+// staged in smem; Y rows stream through a kRing-row cp.async ring (12 rows in
+// flight while 4 are summed), in sorted (= k within a key) order.
+// cols == 32*VEC for VEC in {2, 4}; VEC == 1 handles cols <= 32.
 template <int VEC>
-__global__ void __launch_bounds__(256) sc_fixup(const int32_t* __restrict__ skeys, float* W, int cols,
-                                                int64_t n, const float* __restrict__ carry,
-                                                const ScatterStatus* st) {
+__global__ void __launch_bounds__(kRWarps * 32) sc_reduce(const int32_t* __restrict__ skeys,
+                                                          const int32_t* __restrict__ svals,
+                                                          const float* __restrict__ Y, float* W, int cols,
+                                                          int64_t n, float* carry, int32_t* cfk, int32_t* clk,
+                                                          const ScatterStatus* st) {
   if (*(volatile const int*)&st->flag) return;
-  __shared__ float part[8][128];
+  constexpr int RW = 32 * VEC;   // floats per staged row
+  extern __shared__ __align__(16) float rsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* ring = rsm + (size_t)warp * (kRing * RW + 2 * kChunk);
+  int* kk = reinterpret_cast<int*>(ring + kRing * RW);
+  int* pp = kk + kChunk;
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
-  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const int64_t c0 = c * kChunk, c1 = min(n, c0 + kChunk);
-    const int k0 = __ldg(skeys + c0);
-    const bool first_cont = c0 > 0 && k0 == __ldg(skeys + c0 - 1);
-    if (!first_cont) continue;
-    const bool spans = __ldg(skeys + c1 - 1) == k0 && c1 < n && __ldg(skeys + c1) == k0;
-    if (spans) continue;   // not the chain end
-    // first occurrence of k0
-    int64_t lo = 0, hi = c0;
-    while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if (__ldg(skeys + mid) < k0) lo = mid + 1; else hi = mid;
-    }
-    const int64_t cs = lo / kChunk;   // chain start chunk
-    // chain items: carry[2*cs+1], carry[2*(cs+1)], ..., carry[2*c]
-    const int64_t len = c - cs + 1;
+  const int64_t gw = (int64_t)blockIdx.x * kRWarps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kRWarps;
+  for (int64_t c = gw; c < nchunks; c += nwarps) {
+    const int64_t c0 = c * kChunk;
+    const int cnt = (int)(n - c0 < kChunk ? n - c0 : kChunk);
+#pragma unroll 1
+    for (int j = lane; j < cnt; j += 32) { kk[j] = __ldg(skeys + c0 + j); pp[j] = __ldg(svals + c0 + j); }
+    const int kprev = c0 > 0 ? __ldg(skeys + c0 - 1) : -1;
+    const int knext = c0 + cnt < n ? __ldg(skeys + c0 + cnt) : -2;
+    __syncwarp();
+    if (lane == 0) { cfk[c] = kk[0]; clk[c] = kk[cnt - 1]; }
+    const bool first_cont = kk[0] == kprev;
+    const bool last_cont = kk[cnt - 1] == knext;
+    auto issue = [&](int g) {   // rows 4g .. 4g+3 into their ring slots
+      const int r0 = 4 * g;
+      if (VEC > 1) {   // 16 B per lane
+#pragma unroll
+        for (int t = lane; t < 4 * (RW / 4); t += 32) {
+          const int rr = t / (RW / 4), q = t % (RW / 4);
+          const int j = r0 + rr;
+          if (j < cnt) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(ring + ((j % kRing) * RW) + 4 * q);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+                         "l"(Y + (size_t)pp[j] * cols + 4 * q) : "memory");
+          }
+        }
+      } else {         // cols <= 32: 4 B per lane
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          const int j = r0 + rr;
+          if (j < cnt && lane < cols) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(ring + ((j % kRing) * RW) + lane);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa),
+                         "l"(Y + (size_t)pp[j] * cols + lane) : "memory");
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int ngroups = (cnt + 3) / 4;
+    issue(0);
+    issue(1);
+    issue(2);
     float acc[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
-    for (int64_t i = warp; i < len; i += 8) {
-      const int64_t slot = i == 0 ? 2 * cs + 1 : 2 * (cs + i);
-      float r[VEC];
-      load_row<VEC>(carry + (size_t)slot * cols, cols, lane, r);
+    bool started_before = first_cont;
+#pragma unroll 1
+    for (int g = 0; g < ngroups; ++g) {
+      asm volatile("cp.async.wait_group 2;" ::: "memory");
+      __syncwarp();
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) acc[v] += r[v];
+      for (int u = 0; u < 4; ++u) {
+        const int j = 4 * g + u;
+        if (j < cnt) {
+          const float* r = ring + (j % kRing) * RW;
+#pragma unroll
+          for (int v = 0; v < VEC; ++v)
+            if (VEC > 1 || lane < cols) acc[v] += r[VEC * lane + v];
+          const int key = kk[j];
+          const int next = j + 1 < cnt ? kk[j + 1] : -2;
+          if (next != key) {   // segment ends at entry j
+            const bool continues = next == -2 && last_cont;
+            if (!started_before && !continues) red_row<VEC>(W + (size_t)key * cols, cols, lane, acc);
+            else if (started_before) store_plain<VEC>(carry + (size_t)(2 * c) * cols, cols, lane, acc);
+            else store_plain<VEC>(carry + (size_t)(2 * c + 1) * cols, cols, lane, acc);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
+            started_before = false;
+          }
+        }
+      }
+      __syncwarp();   // the ring slots of group g are free again
+      issue(g + 3);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+}
+
+// Chains of chunk partials for segments that cross chunk boundaries.  Warp w
+// of block b checks chunk c = 8b + w.  If c ends a chain (its first segment
+// started earlier and ends inside c): a 2-chunk chain is summed by the warp
+// (carry[2(c-1)+1] + carry[2c]); a longer chain (a hot row spanning whole
+// chunks) is queued and summed by the whole block in chunk order with a fixed
+// tree, after a binary search over the per-chunk last keys for its start.
+template <int VEC>
+__global__ void __launch_bounds__(256) sc_fixup(float* W, int cols, int64_t n, const float* __restrict__ carry,
+                                                const int32_t* __restrict__ cfk, const int32_t* __restrict__ clk,
+                                                const ScatterStatus* st) {
+  if (*(volatile const int*)&st->flag) return;
+  __shared__ float part[8][128];
+  __shared__ long long lq[8];
+  __shared__ int nl;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  if (threadIdx.x == 0) nl = 0;
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * 8 + warp;
+  if (c > 0 && c < nchunks) {
+    const int k0 = __ldcg(cfk + c);
+    const bool first_cont = k0 == __ldcg(clk + c - 1);
+    const bool spans = __ldcg(clk + c) == k0 && c + 1 < nchunks && __ldcg(cfk + c + 1) == k0;
+    if (first_cont && !spans) {
+      if (__ldcg(cfk + c - 1) != k0) {   // chain = (c-1, c)
+        float a[VEC], b2[VEC];
+        load_row<VEC>(carry + (size_t)(2 * (c - 1) + 1) * cols, cols, lane, a);
+        load_row<VEC>(carry + (size_t)(2 * c) * cols, cols, lane, b2);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) a[v] += b2[v];
+        red_row<VEC>(W + (size_t)k0 * cols, cols, lane, a);
+      } else if (lane == 0) {
+        lq[atomicAdd(&nl, 1)] = c;
+      }
+    }
+  }
+  __syncthreads();
+  const int nlong = nl;
+  for (int qi = 0; qi < nlong; ++qi) {
+    const int64_t ce = lq[qi];
+    const int k0 = __ldcg(cfk + ce);
+    // chain start: the chunk before the run of chunks whose first key is k0
+    // (all chunks ce-1, ce-2, ... start with k0); 256 chunks per round trip
+    __shared__ long long s_cs;
+    if (threadIdx.x == 0) s_cs = -1;
+    __syncthreads();
+    for (int64_t top = ce - 1; ; top -= 256) {
+      const int64_t ci = top - threadIdx.x;
+      const bool brk = ci >= 0 && __ldcg(cfk + ci) != k0;   // chunk ci does not start with k0
+      const int any = __syncthreads_or(brk);
+      if (brk) atomicMax(&s_cs, (long long)ci);
+      __syncthreads();
+      if (any || top - 255 <= 0) break;
+    }
+    int64_t cs = s_cs < 0 ? 0 : s_cs;
+    if (__ldcg(clk + cs) != k0) ++cs;   // k0 starts exactly at chunk cs+1's first entry
+    // chain items: carry[2*cs+1], carry[2*(cs+1)], ..., carry[2*ce]; warp w
+    // sums the contiguous part [len*w/8, len*(w+1)/8) in order, 8 loads in flight
+    const int64_t len = ce - cs + 1;
+    const int64_t i0 = len * warp / 8, i1 = len * (warp + 1) / 8;
+    float acc[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
+    for (int64_t ib = i0; ib < i1; ib += 8) {
+      float r[8][VEC];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t i = ib + k;
+        const int64_t slot = i == 0 ? 2 * cs + 1 : 2 * (cs + i);
+        if (i < i1) load_row<VEC>(carry + (size_t)slot * cols, cols, lane, r[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (ib + k < i1)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc[v] += r[k][v];
     }
 #pragma unroll
     for (int v = 0; v < VEC; ++v) part[warp][lane * VEC + v] = acc[v];
     __syncthreads();
     if (warp == 0) {
-      float s[VEC];
+      float sacc[VEC];
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) s[v] = part[0][lane * VEC + v];
+      for (int v = 0; v < VEC; ++v) sacc[v] = part[0][lane * VEC + v];
       for (int w = 1; w < 8; ++w)
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) s[v] += part[w][lane * VEC + v];
-      store_rmw<VEC>(W + (size_t)k0 * cols, cols, lane, s);
+        for (int v = 0; v < VEC; ++v) sacc[v] += part[w][lane * VEC + v];
+      red_row<VEC>(W + (size_t)k0 * cols, cols, lane, sacc);
     }
     __syncthreads();
   }
 }
-
 // ------------------------------------------------------------------ atomic path
 __global__ void sc_validate(const int32_t* __restrict__ I, int64_t n, int64_t rows, ScatterStatus* st) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -366,25 +511,26 @@ static int bits_for(int64_t rows) {
 ScatterPlan scatter_plan(int64_t rows, int cols, int64_t n, int num_sms) {
   ScatterPlan pl{};
   const int nb = bits_for(rows);
-  pl.passes = (nb + 10) / 11;
+  pl.passes = (nb + kMaxDigitBits - 1) / kMaxDigitBits;
   pl.bits = (nb + pl.passes - 1) / pl.passes;
   pl.bins = 1 << pl.bits;
   pl.ntiles = (n + kSortTile - 1) / kSortTile;
   pl.nchunks = (n + kChunk - 1) / kChunk;
   pl.num_sms = num_sms;
-  // workspace layout (bytes)
   size_t o = 0;
   auto take = [&](size_t b) { size_t r = o; o += (b + 255) & ~size_t(255); return r; };
   pl.off_status = take(sizeof(ScatterStatus));
-  pl.off_hist = take(sizeof(int) * pl.passes * pl.bins);
-  pl.off_ctr = take(sizeof(unsigned) * 4);
-  pl.off_lookback = take(sizeof(unsigned) * pl.passes * pl.ntiles * pl.bins);
-  pl.zero_bytes = o;   // everything above is zeroed per call
+  pl.zero_bytes = o;   // only the status block is reset per call
+  pl.off_hist = take(sizeof(int) * pl.bins * pl.ntiles);   // digit-major tile counts
+  pl.off_ctr = take(sizeof(int) * kScanBlocks);
+  pl.off_lookback = take(16);
   pl.off_ka = take(sizeof(int) * n);
   pl.off_va = take(sizeof(int) * n);
   pl.off_kb = take(sizeof(int) * n);
   pl.off_vb = take(sizeof(int) * n);
   pl.off_carry = take(sizeof(float) * 2 * pl.nchunks * cols);
+  pl.off_cfk = take(sizeof(int) * pl.nchunks);
+  pl.off_clk = take(sizeof(int) * pl.nchunks);
   pl.total_bytes = o;
   return pl;
 }
@@ -401,6 +547,12 @@ int scatter_supported(int cols, int mode) {
   return 1;
 }
 
+static size_t reduce_smem(int vec) { return sizeof(float) * kRWarps * (kRing * 32 * vec + 2 * kChunk); }
+
+static size_t downsweep_smem(int bins) {
+  return sizeof(int) * ((kSortThreads / 32) * bins + 2 * bins + 2 * kSortTile);
+}
+
 cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t rows, int cols,
                            const float* Y, const int32_t* I, int64_t n, int mode, cudaStream_t s,
                            int* launches) {
@@ -408,8 +560,7 @@ cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t ro
   ScatterStatus* st = reinterpret_cast<ScatterStatus*>(b + pl.off_status);
   cudaError_t e = cudaMemsetAsync(b, 0, pl.zero_bytes, s);
   if (e != cudaSuccess) return e;
-  // bad starts at "none"
-  e = cudaMemsetAsync(&st->bad, 0xff, sizeof(st->bad), s);
+  e = cudaMemsetAsync(&st->bad, 0xff, sizeof(st->bad), s);   // "no bad index"
   if (e != cudaSuccess) return e;
   const int blocks = pl.num_sms * 4;
   if (mode == 1) {
@@ -419,43 +570,48 @@ cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t ro
     *launches += 2;
     return cudaGetLastError();
   }
-  int* hist = reinterpret_cast<int*>(b + pl.off_hist);
-  unsigned* ctr = reinterpret_cast<unsigned*>(b + pl.off_ctr);
-  unsigned* lb = reinterpret_cast<unsigned*>(b + pl.off_lookback);
+  int* counts = reinterpret_cast<int*>(b + pl.off_hist);
+  int* bsum = reinterpret_cast<int*>(b + pl.off_ctr);
   int32_t* ka = reinterpret_cast<int32_t*>(b + pl.off_ka);
   int32_t* va = reinterpret_cast<int32_t*>(b + pl.off_va);
   int32_t* kb = reinterpret_cast<int32_t*>(b + pl.off_kb);
   int32_t* vb = reinterpret_cast<int32_t*>(b + pl.off_vb);
   float* carry = reinterpret_cast<float*>(b + pl.off_carry);
-  sc_hist<<<blocks, 512, sizeof(int) * pl.passes * pl.bins, s>>>(I, n, rows, pl.passes, pl.bits, hist, st);
-  *launches += 1;
-  const size_t sm = sizeof(int) * (8 * pl.bins + pl.bins + 32);
+  int32_t* cfk = reinterpret_cast<int32_t*>(b + pl.off_cfk);
+  int32_t* clk = reinterpret_cast<int32_t*>(b + pl.off_clk);
+  const size_t smu = sizeof(int) * (kSortThreads / 32) * pl.bins;
+  const size_t smd = downsweep_smem(pl.bins);
+  const int m = (int)(pl.bins * pl.ntiles);
   const int32_t* kin = I;
   const int32_t* vin = nullptr;
   for (int p = 0; p < pl.passes; ++p) {
     int32_t* ko = (p & 1) ? kb : ka;
     int32_t* vo = (p & 1) ? vb : va;
-    sc_onesweep<<<(unsigned)pl.ntiles, kSortThreads, sm, s>>>(
-        kin, vin, ko, vo, n, p * pl.bits, pl.bits, hist + p * pl.bins,
-        lb + (size_t)p * pl.ntiles * pl.bins, ctr + p, st);
-    *launches += 1;
+    sc_upsweep<<<(unsigned)pl.ntiles, kSortThreads, smu, s>>>(kin, n, p * pl.bits, pl.bits, p == 0 ? rows : 0,
+                                                               counts, st);
+    sc_scan_reduce<<<kScanBlocks, 256, 0, s>>>(counts, m, bsum, st);
+    sc_scan_apply<<<kScanBlocks, 256, 0, s>>>(counts, m, bsum, st);
+    sc_downsweep<<<(unsigned)pl.ntiles, kSortThreads, smd, s>>>(kin, vin, ko, vo, n, p * pl.bits, pl.bits, counts,
+                                                                 st);
+    *launches += 4;
     kin = ko;
     vin = vo;
   }
   const int vec = vec_for(cols);
-  const int rblocks = (int)((pl.nchunks * 32 + 255) / 256);
+  const int rblocks = (int)((pl.nchunks + kRWarps - 1) / kRWarps);
+  const int fblocks = (int)((pl.nchunks + 7) / 8);
   switch (vec) {
     case 4:
-      sc_reduce<4><<<rblocks, 256, 0, s>>>(kin, vin, Y, W, cols, n, carry, st);
-      sc_fixup<4><<<blocks, 256, 0, s>>>(kin, W, cols, n, carry, st);
+      sc_reduce<4><<<rblocks, kRWarps * 32, reduce_smem(4), s>>>(kin, vin, Y, W, cols, n, carry, cfk, clk, st);
+      sc_fixup<4><<<fblocks, 256, 0, s>>>(W, cols, n, carry, cfk, clk, st);
       break;
     case 2:
-      sc_reduce<2><<<rblocks, 256, 0, s>>>(kin, vin, Y, W, cols, n, carry, st);
-      sc_fixup<2><<<blocks, 256, 0, s>>>(kin, W, cols, n, carry, st);
+      sc_reduce<2><<<rblocks, kRWarps * 32, reduce_smem(2), s>>>(kin, vin, Y, W, cols, n, carry, cfk, clk, st);
+      sc_fixup<2><<<fblocks, 256, 0, s>>>(W, cols, n, carry, cfk, clk, st);
       break;
     default:
-      sc_reduce<1><<<rblocks, 256, 0, s>>>(kin, vin, Y, W, cols, n, carry, st);
-      sc_fixup<1><<<blocks, 256, 0, s>>>(kin, W, cols, n, carry, st);
+      sc_reduce<1><<<rblocks, kRWarps * 32, reduce_smem(1), s>>>(kin, vin, Y, W, cols, n, carry, cfk, clk, st);
+      sc_fixup<1><<<fblocks, 256, 0, s>>>(W, cols, n, carry, cfk, clk, st);
       break;
   }
   *launches += 2;
@@ -463,8 +619,16 @@ cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t ro
 }
 
 cudaError_t scatter_prepare(int bins) {
-  const size_t sm = sizeof(int) * (8 * bins + bins + 32);
-  return cudaFuncSetAttribute(sc_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = cudaFuncSetAttribute(sc_downsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)downsweep_smem(bins));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sc_upsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(int) * (kSortThreads / 32) * bins));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sc_reduce<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reduce_smem(4));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sc_reduce<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reduce_smem(2));
+  return e;
 }
 
 }  // namespace pg
