@@ -194,10 +194,8 @@ def main():
     model = pg.PolyglotModel(V, d, n, h, seed=42, scatter=1 if args.scatter == "atomic" else 0,
                              stream=stream)
     if world > 1:
-        uid = pg.pg_nccl_unique_id() if rank == 0 else bytes(128)
-        t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).to(dev)
-        dist.broadcast(t, 0)
-        model.attach_nccl(rank, world, bytes(t.cpu().numpy()))
+        from paper_1404_1521_b200 import dp
+        dp.attach(model, rank, world, dev)   # library-owned NCCL communicator
     model.reserve(B)
     total = args.warmup + args.steps
     # per-step synthetic batches, rank-specific substreams, resident in HBM
@@ -272,7 +270,7 @@ def main():
            "h2d_bytes_per_step": B * n * 4 + B * 4, "d2h_bytes_per_step": 80}
 
     extras = {}
-    if not args.no_extras and rank == 0:
+    if not args.no_extras and world == 1:
         extras = run_extras(pg, torch, synth, np, dev, stream, flush, model)
 
     if rank == 0:

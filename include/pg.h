@@ -158,6 +158,17 @@ pg_status pg_nccl_unique_id(void* out_128_bytes);
 pg_status pg_attach_nccl(pg_model* m, int rank, int world,
                          const void* nccl_unique_id_128_bytes);
 
+/* pg_train_step_group -- `world` replicas of one model on ONE device take one
+ * data-parallel step together: replica r trains on windows
+ * idx_all[r*batch_local .. (r+1)*batch_local) (contiguous shards), the per-
+ * replica records are exchanged by device copies instead of NCCL, and every
+ * replica applies the same update (the arithmetic of the NCCL path, for tests
+ * and single-GPU emulation of G ranks).  loss_out (host, may be NULL) gets the
+ * global mean loss.  Models used here must not also be attached to NCCL. */
+pg_status pg_train_step_group(pg_model** models, int world, const int32_t* idx_all,
+                              const int32_t* corr_all, int32_t batch_local, float lr,
+                              float* loss_out);
+
 /* Number of kernels the library launched since the model was created
  * (counts host-side launches; graph replays are not counted). */
 int64_t pg_kernel_launches(const pg_model* m);

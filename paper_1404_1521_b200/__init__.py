@@ -30,7 +30,7 @@ EXPORTED = [
     "pg_init", "pg_train_step", "pg_train_step_loss", "pg_score", "pg_free", "pg_last_error",
     "pg_get_params", "pg_set_params", "pg_get_shape", "pg_set_option", "pg_sync",
     "pg_scatter_add", "pg_scatter_add_async", "pg_nccl_unique_id", "pg_attach_nccl",
-    "pg_kernel_launches", "pg_abi_version",
+    "pg_kernel_launches", "pg_abi_version", "pg_train_step_group",
 ]
 
 _lib = None
@@ -68,6 +68,7 @@ def lib():
             "pg_attach_nccl": ([P, ctypes.c_int, ctypes.c_int, P], ctypes.c_int),
             "pg_kernel_launches": ([P], i64),
             "pg_abi_version": ([], ctypes.c_int),
+            "pg_train_step_group": ([P, ctypes.c_int, P, P, i32, f32, P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -286,3 +287,16 @@ def pg_abi_version() -> int:
 
 def pg_scatter_add_async(W, Y, I, mode=PG_SCATTER_DET, stream=None, err_flag=None):
     return pg_scatter_add(W, Y, I, mode, stream, blocking=False, err_flag=err_flag)
+
+
+def pg_train_step_group(handles, idx_all, corr_all, lr):
+    """One data-parallel step of len(handles) replicas on one device (contiguous
+    shards of idx_all / corr_all); returns the global mean loss."""
+    world = len(handles)
+    arr = (ctypes.c_void_p * world)(*[h.value if hasattr(h, "value") else h for h in handles])
+    batch_local = int(corr_all.shape[0]) // world
+    out = ctypes.c_float()
+    _check(lib().pg_train_step_group(ctypes.cast(arr, ctypes.c_void_p), world, _ptr(idx_all, np.int32),
+                                     _ptr(corr_all, np.int32), batch_local, float(lr),
+                                     ctypes.cast(ctypes.byref(out), ctypes.c_void_p)), "pg_train_step_group")
+    return out.value

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/pg.h"
 #include "common.cuh"
@@ -70,9 +71,17 @@ struct pg_model {
   // data parallel
   int rank = 0, world = 1;
   void* comm = nullptr;
-  float* dp_send = nullptr;   // [rank record]
-  float* dp_recv = nullptr;   // [world][rank record]
-  size_t dp_rec_floats = 0;
+  // data-parallel records: send = this rank's, recv = [world][...] gathered
+  float* send_dense = nullptr;
+  int32_t* send_off = nullptr;
+  int32_t* send_rows = nullptr;
+  float* send_vals = nullptr;
+  float* recv_dense = nullptr;
+  int32_t* recv_off = nullptr;
+  int32_t* recv_rows = nullptr;
+  float* recv_vals = nullptr;
+  int64_t dp_cap_B = 0;
+  bool emulated = false;   // group of replicas on one device (pg_train_step_group)
 };
 
 // ------------------------------------------------------------------ init kernel
@@ -142,6 +151,14 @@ static PtrKind ptr_kind(const void* p) {
   return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? PTR_DEVICE : PTR_HOST;
 }
 
+static void free_dp(pg_model* m) {
+  cudaFree(m->send_dense); cudaFree(m->send_off); cudaFree(m->send_rows); cudaFree(m->send_vals);
+  cudaFree(m->recv_dense); cudaFree(m->recv_off); cudaFree(m->recv_rows); cudaFree(m->recv_vals);
+  m->send_dense = m->recv_dense = m->send_vals = m->recv_vals = nullptr;
+  m->send_off = m->send_rows = m->recv_off = m->recv_rows = nullptr;
+  m->dp_cap_B = 0;
+}
+
 static void free_ws(pg_model* m) {
   cudaFree(m->dense_part); cudaFree(m->list_rows); cudaFree(m->list_vals); cudaFree(m->list_off);
   m->dense_part = nullptr; m->list_rows = nullptr; m->list_vals = nullptr; m->list_off = nullptr;
@@ -163,7 +180,7 @@ static Geometry geometry(const pg_model* m, int B) {
   g.cap = (m->n + 1) * g.T;
   g.NL = g.P * g.R;
   g.dense_len = m->n * m->d * m->h + 2 * m->h;
-  g.dense_stride = ((g.dense_len + 1) + 3) & ~3;
+  g.dense_stride = ((g.dense_len + 2) + 3) & ~3;   // dense | hinge | flags
   g.lay = make_layout(m->d, m->n, m->h, g.T, step_block_threads(m->d, m->n, m->h, m->fast), g.NL * m->world,
                       m->fast);
   g.smem = (size_t)(g.lay.total1 > g.lay.total2 ? g.lay.total1 : g.lay.total2);
@@ -174,8 +191,8 @@ static pg_status ensure_ws(pg_model* m, int B) {
   Geometry g = geometry(m, B);
   if (g.smem > m->smem_max)
     return fail(PG_EINVAL, "batch %d needs %zu B of shared memory per CTA (max %zu)", B, g.smem, m->smem_max);
-  const int64_t lists = (int64_t)g.NL * m->world;
-  const int64_t dense = (int64_t)g.P * m->world * g.dense_stride;
+  const int64_t lists = (int64_t)g.NL;
+  const int64_t dense = (int64_t)g.P * g.dense_stride;
   const int64_t off = lists * (g.P + 1);
   if (lists * g.cap > m->cap_lists || dense > m->cap_dense || off > m->cap_off) {
     CU(cudaStreamSynchronize(m->stream));
@@ -186,6 +203,20 @@ static pg_status ensure_ws(pg_model* m, int B) {
     CU(cudaMalloc(&m->list_vals, sizeof(float) * L * m->d));
     CU(cudaMalloc(&m->list_off, sizeof(int32_t) * off));
     m->cap_lists = L; m->cap_dense = dense; m->cap_off = off;
+  }
+  if (m->world > 1 && B != m->dp_cap_B) {   // record sizes depend on the exact local batch
+    CU(cudaStreamSynchronize(m->stream));
+    free_dp(m);
+    const int64_t W = m->world, cap = (int64_t)(m->n + 1) * B, offn = (int64_t)g.NL * (g.P + 1);
+    CU(cudaMalloc(&m->send_dense, sizeof(float) * g.dense_stride));
+    CU(cudaMalloc(&m->send_off, sizeof(int32_t) * offn));
+    CU(cudaMalloc(&m->send_rows, sizeof(int32_t) * cap));
+    CU(cudaMalloc(&m->send_vals, sizeof(float) * cap * m->d));
+    CU(cudaMalloc(&m->recv_dense, sizeof(float) * g.dense_stride * W));
+    CU(cudaMalloc(&m->recv_off, sizeof(int32_t) * offn * W));
+    CU(cudaMalloc(&m->recv_rows, sizeof(int32_t) * cap * W));
+    CU(cudaMalloc(&m->recv_vals, sizeof(float) * cap * m->d * W));
+    m->dp_cap_B = B;
   }
   if (B > m->cap_in) {
     CU(cudaStreamSynchronize(m->stream));
@@ -209,6 +240,8 @@ static pg_status set_device(const pg_model* m) {
 }
 
 static pg_status status_from_flags(int flags, unsigned long long bad, const char* what) {
+  if ((flags & 1) && bad == kNoBad)
+    return fail(PG_ERANGE, "%s: index out of range on another rank; no parameter was modified", what);
   if (flags & 1) {
     const long long pos = (long long)(bad >> 32);
     const int val = (int)(unsigned)(bad & 0xffffffffull);
@@ -285,7 +318,7 @@ extern "C" void pg_free(pg_model* m) {
   cudaFree(m->C); cudaFree(m->W1); cudaFree(m->b1); cudaFree(m->w2); cudaFree(m->b2);
   cudaFree(m->st); cudaFreeHost(m->st_host);
   cudaFree(m->d_idx); cudaFree(m->d_corr); cudaFree(m->d_scores);
-  cudaFree(m->dp_send); cudaFree(m->dp_recv);
+  free_dp(m);
   delete m;
 }
 
@@ -480,6 +513,14 @@ static StepParams make_params(pg_model* m, const Geometry& g, const int32_t* idx
   p.loss_out = loss_dev;
   p.mode = m->mode;
   p.smem_bytes = (int)g.smem;
+  p.LPR = g.NL;
+  p.list_stride = g.cap;
+  p.rank_stride = 0;
+  p.flags_from_records = 0;
+  p.send_dense = m->send_dense;
+  p.send_off = m->send_off;
+  p.send_rows = m->send_rows;
+  p.send_vals = m->send_vals;
   p.lay = g.lay;
   p.trace = m->trace;
   return p;
@@ -491,7 +532,7 @@ static pg_status run_step(pg_model* m, const int32_t* idx, const int32_t* corr, 
                           float* loss_dev) {
   const Geometry g = geometry(m, B);
   StepParams p = make_params(m, g, idx, corr, B, lr, loss_dev);
-  if (m->world > 1) return dp_step(m, g, p);
+  if (m->world > 1 && !m->emulated) return dp_step(m, g, p);
   int l = 0;
   launch_step(p, m->fused, m->fast, m->stream, &l);
   m->launches += l;
@@ -500,9 +541,116 @@ static pg_status run_step(pg_model* m, const int32_t* idx, const int32_t* corr, 
 }
 
 // ------------------------------------------------------------------ data parallel (NCCL)
+// Phase 2 parameters over the gathered records of `world` ranks.
+static StepParams record_params(const pg_model* m, const Geometry& g, const StepParams& p) {
+  StepParams q = p;
+  const int W = m->world;
+  q.dense_part = m->recv_dense;
+  q.dense_stride = g.dense_stride;
+  q.Ptot = W;
+  q.list_off = m->recv_off;
+  q.list_rows = m->recv_rows;
+  q.list_vals = m->recv_vals;
+  q.NLtot = g.NL * W;
+  q.LPR = g.NL;
+  q.list_stride = 0;
+  q.rank_stride = (m->n + 1) * p.B;
+  q.flags_from_records = 1;
+  return q;
+}
+
+// Data-parallel step: phase 1 + this rank's compact record in
+// one cooperative kernel, one grouped NCCL all-gather of the records, then the
+// same phase 2 over all ranks' records on every rank -- identical inputs in an
+// identical order, so replicas stay bit-identical in DET mode.
 pg_status dp_step(pg_model* m, const Geometry& g, StepParams& p) {
-  (void)g; (void)p;
-  return fail(PG_ENCCL, "data-parallel step not available in this build");
+  if (!m->comm) return fail(PG_ENCCL, "data-parallel step without a communicator");
+  int l = 0;
+  launch_step_phases(p, 1 | 4, m->fast, m->stream, &l);
+  CU(cudaGetLastError());
+  const int64_t cap = (int64_t)(m->n + 1) * p.B, offn = (int64_t)g.NL * (g.P + 1);
+  std::string err;
+  if (nccl_shim_group(true, &err) ||
+      nccl_shim_allgather_f32(m->send_dense, m->recv_dense, (size_t)g.dense_stride, m->comm, m->stream, &err) ||
+      nccl_shim_allgather_f32(reinterpret_cast<float*>(m->send_off), reinterpret_cast<float*>(m->recv_off),
+                              (size_t)offn, m->comm, m->stream, &err) ||
+      nccl_shim_allgather_f32(reinterpret_cast<float*>(m->send_rows), reinterpret_cast<float*>(m->recv_rows),
+                              (size_t)cap, m->comm, m->stream, &err) ||
+      nccl_shim_allgather_f32(m->send_vals, m->recv_vals, (size_t)(cap * m->d), m->comm, m->stream, &err) ||
+      nccl_shim_group(false, &err))
+    return fail(PG_ENCCL, "%s", err.c_str());
+  const StepParams q = record_params(m, g, p);
+  launch_step_phases(q, 2, m->fast, m->stream, &l);
+  m->launches += l;
+  CU(cudaGetLastError());
+  return PG_OK;
+}
+
+// Replicas of one model on ONE device exchanging records by device copies: the
+// data-parallel arithmetic of dp_step without NCCL (tests, single-GPU runs).
+extern "C" pg_status pg_train_step_group(pg_model** ms, int world, const int32_t* idx_all,
+                                         const int32_t* corr_all, int32_t batch_local, float lr,
+                                         float* loss_out) {
+  if (!ms || world < 1) return fail(PG_EINVAL, "pg_train_step_group: bad arguments");
+  if (!idx_all || !corr_all) return fail(PG_EINVAL, "pg_train_step_group: null index pointer");
+  if (batch_local < 1) return fail(PG_EINVAL, "pg_train_step_group: empty batch");
+  if (!std::isfinite(lr) || !(lr > 0.f)) return fail(PG_EINVAL, "pg_train_step_group: lr must be finite and > 0");
+  for (int r = 0; r < world; ++r) {
+    if (pg_status s = check_model(ms[r])) return s;
+    if (ms[r]->comm) return fail(PG_EINVAL, "pg_train_step_group: model %d has an NCCL communicator", r);
+    if (ms[r]->d != ms[0]->d || ms[r]->n != ms[0]->n || ms[r]->h != ms[0]->h || ms[r]->V != ms[0]->V)
+      return fail(PG_EINVAL, "pg_train_step_group: shape mismatch");
+    if (ms[r]->world != world) { ms[r]->world = world; ms[r]->rank = r; free_ws(ms[r]); free_dp(ms[r]); }
+    ms[r]->emulated = true;
+    if (pg_status s = set_device(ms[r])) return s;
+    if (pg_status s = ensure_ws(ms[r], batch_local)) return s;
+  }
+  pg_model* m0 = ms[0];
+  const int n = m0->n;
+  const Geometry g = geometry(m0, batch_local);
+  // phase 1 + records, one replica after another on replica 0's stream
+  std::vector<StepParams> ps(world);
+  for (int r = 0; r < world; ++r) {
+    pg_model* m = ms[r];
+    const int32_t *di = nullptr, *dc = nullptr;
+    m->stream = m0->stream;
+    if (pg_status s = stage_inputs(m, idx_all + (size_t)r * batch_local * n, corr_all + (size_t)r * batch_local,
+                                   batch_local, &di, &dc))
+      return s;
+    ps[r] = make_params(m, g, di, dc, batch_local, lr, nullptr);
+    int l = 0;
+    launch_step_phases(ps[r], 1 | 4, m->fast, m->stream, &l);
+    m->launches += l;
+    CU(cudaGetLastError());
+  }
+  // "all-gather": every replica receives every replica's record
+  const int64_t cap = (int64_t)(n + 1) * batch_local, offn = (int64_t)g.NL * (g.P + 1);
+  for (int dst = 0; dst < world; ++dst)
+    for (int src = 0; src < world; ++src) {
+      pg_model* a = ms[dst];
+      pg_model* b = ms[src];
+      cudaStream_t s = m0->stream;
+      CU(cudaMemcpyAsync(a->recv_dense + (size_t)src * g.dense_stride, b->send_dense, sizeof(float) * g.dense_stride,
+                         cudaMemcpyDeviceToDevice, s));
+      CU(cudaMemcpyAsync(a->recv_off + (size_t)src * offn, b->send_off, sizeof(int32_t) * offn,
+                         cudaMemcpyDeviceToDevice, s));
+      CU(cudaMemcpyAsync(a->recv_rows + (size_t)src * cap, b->send_rows, sizeof(int32_t) * cap,
+                         cudaMemcpyDeviceToDevice, s));
+      CU(cudaMemcpyAsync(a->recv_vals + (size_t)src * cap * a->d, b->send_vals, sizeof(float) * cap * a->d,
+                         cudaMemcpyDeviceToDevice, s));
+    }
+  for (int r = 0; r < world; ++r) {
+    const StepParams q = record_params(ms[r], g, ps[r]);
+    int l = 0;
+    launch_step_phases(q, 2, ms[r]->fast, m0->stream, &l);
+    ms[r]->launches += l;
+    CU(cudaGetLastError());
+  }
+  if (!loss_out) return PG_OK;
+  CU(cudaMemcpyAsync(m0->st_host, m0->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, m0->stream));
+  CU(cudaStreamSynchronize(m0->stream));
+  *loss_out = m0->st_host->last_loss;
+  return status_from_flags(m0->st_host->rank_flags, m0->st_host->last_bad, "pg_train_step_group");
 }
 
 extern "C" pg_status pg_nccl_unique_id(void* out) {

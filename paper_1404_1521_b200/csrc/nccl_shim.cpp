@@ -14,6 +14,8 @@ struct Api {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
 };
 Api g_api;
@@ -33,8 +35,11 @@ void load() {
   g_api.commInitRank = (decltype(g_api.commInitRank))dlsym(g_api.h, "ncclCommInitRank");
   g_api.allGather = (decltype(g_api.allGather))dlsym(g_api.h, "ncclAllGather");
   g_api.commDestroy = (decltype(g_api.commDestroy))dlsym(g_api.h, "ncclCommDestroy");
+  g_api.groupStart = (decltype(g_api.groupStart))dlsym(g_api.h, "ncclGroupStart");
+  g_api.groupEnd = (decltype(g_api.groupEnd))dlsym(g_api.h, "ncclGroupEnd");
   g_api.getErrorString = (decltype(g_api.getErrorString))dlsym(g_api.h, "ncclGetErrorString");
-  if (!g_api.getUniqueId || !g_api.commInitRank || !g_api.allGather || !g_api.commDestroy)
+  if (!g_api.getUniqueId || !g_api.commInitRank || !g_api.allGather || !g_api.commDestroy || !g_api.groupStart ||
+      !g_api.groupEnd)
     g_load_err = "libnccl.so.2 lacks required symbols";
 }
 
@@ -77,4 +82,9 @@ int nccl_shim_allgather_f32(const float* send, float* recv, size_t count, void* 
 int nccl_shim_destroy(void* comm) {
   if (!comm || !ready(nullptr)) return 1;
   return g_api.commDestroy(static_cast<ncclComm_t>(comm)) != ncclSuccess;
+}
+
+int nccl_shim_group(bool start, std::string* err) {
+  if (!ready(err)) return 1;
+  return check(start ? g_api.groupStart() : g_api.groupEnd(), start ? "ncclGroupStart" : "ncclGroupEnd", err);
 }

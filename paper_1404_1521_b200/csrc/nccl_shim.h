@@ -12,3 +12,4 @@ int nccl_shim_init(void** comm, int rank, int world, const void* uid128, std::st
 int nccl_shim_allgather_f32(const float* send, float* recv, size_t count, void* comm, cudaStream_t s,
                             std::string* err);
 int nccl_shim_destroy(void* comm);
+int nccl_shim_group(bool start, std::string* err);

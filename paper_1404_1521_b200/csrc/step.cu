@@ -39,6 +39,10 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
+__device__ __forceinline__ size_t list_index(const StepParams& p, int L, int off) {
+  return (size_t)(L / p.LPR) * p.rank_stride + (size_t)(L % p.LPR) * p.list_stride + off;
+}
+
 // Optional phase timestamps for profiling (PG_OPT_TRACE; thread 0 of each CTA).
 __device__ __forceinline__ void trace_mark(const StepParams& p, int k) {
   if (p.trace != nullptr && threadIdx.x == 0) {
@@ -702,7 +706,7 @@ __device__ __forceinline__ int dense_groups(int nq, int NT) {
 
 // Combine the groups (in order) and apply W1/b1/w2 -= lr * grad for one block.
 __device__ __forceinline__ void dense_apply(const StepParams& p, unsigned char* sm, int qb, int nq, int groups, float4 acc,
-                                         float4 cur4, bool write) {
+                                         float4 cur4, bool write, float* sums_out = nullptr) {
   const float cur[4] = {cur4.x, cur4.y, cur4.z, cur4.w};
   const int tid = threadIdx.x, ndh = p.n * p.d * p.h, DL = p.dense_len;
   float4* dred = reinterpret_cast<float4*>(sm + p.lay.dred);
@@ -718,7 +722,11 @@ __device__ __forceinline__ void dense_apply(const StepParams& p, unsigned char* 
     }
     const float sv[4] = {s.x, s.y, s.z, s.w};
     const int base = 4 * (qb + tid);
-    if (write) {
+    if (sums_out) {   // data-parallel record: this rank's summed dense gradient
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (base + k < DL) sums_out[base + k] = sv[k];
+    } else if (write) {
       if ((ndh & 3) == 0 && (p.h & 3) == 0) {   // a quad never straddles W1 | b1 | w2
         float* q = param_ptr(p, base, ndh);
 #pragma unroll
@@ -787,9 +795,9 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
             if (lbase[mid] <= base + e) lo = mid; else hi = mid - 1;
           }
           const int L = lo;
-          const int j = loff[L] + (base + e - lbase[L]);
-          const unsigned row = (unsigned)__ldcg(p.list_rows + (size_t)L * p.cap + j);
-          keys[e] = ((unsigned long long)row << 32) | ((unsigned long long)L << 8) | (unsigned)j;
+          const int rel = base + e - lbase[L];   // offset inside the owner bucket (< 256)
+          const unsigned row = (unsigned)__ldcg(p.list_rows + list_index(p, L, loff[L] + rel));
+          keys[e] = ((unsigned long long)row << 32) | ((unsigned long long)L << 8) | (unsigned)rel;
         } else {
           keys[e] = ~0ull;
         }
@@ -809,15 +817,16 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
       }
       if (tid == 0) seg[nseg_total] = Mw;
       __syncthreads();
+      int par = 0;   // carry double buffer: read carry[par], write carry[par ^ 1]
       #pragma unroll 1
-      for (int sb0 = 0; sb0 < Mw; sb0 += lay.SB) {
+      for (int sb0 = 0; sb0 < Mw; sb0 += lay.SB, par ^= 1) {
         const int sb1 = min(Mw, sb0 + lay.SB);
         #pragma unroll 1
         for (int t = tid; t < (sb1 - sb0) * d; t += NT) {
           const int e = sb0 + t / d, f = t % d;
           const unsigned long long k = keys[e];
-          const int L = (int)((k >> 8) & 0xffffff), j = (int)(k & 0xff);
-          stage[t] = __ldcg(p.list_vals + ((size_t)L * p.cap + j) * d + f);
+          const int L = (int)((k >> 8) & 0xffffff), rel = (int)(k & 0xff);
+          stage[t] = __ldcg(p.list_vals + list_index(p, L, loff[L] + rel) * d + f);
         }
         __syncthreads();
         int slo = 0, shi = nseg_total - 1;
@@ -833,14 +842,14 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
           const unsigned row = (unsigned)(keys[s0] >> 32);
           #pragma unroll 1
           for (int f = lane; f < d; f += 32) {
-            float acc = cont ? carry[f] : 0.f;
+            float acc = cont ? carry[par * d + f] : 0.f;
             #pragma unroll 1
             for (int e = a0; e < a1; ++e) acc += stage[(e - sb0) * d + f];
             if (fin) {
               float* cp = p.C + (size_t)row * d + f;
               *cp = __ldcg(cp) + nlr * acc;
             } else {
-              carry[f] = acc;
+              carry[(par ^ 1) * d + f] = acc;
             }
           }
         }
@@ -912,7 +921,7 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
       const int mid = (lo + hi + 1) >> 1;
       if (lbase[mid] <= e) lo = mid; else hi = mid - 1;
     }
-    esrc[e] = lo * p.cap + loff[lo] + (e - lbase[lo]);
+    esrc[e] = (int)list_index(p, lo, loff[lo] + (e - lbase[lo]));
   }
   #pragma unroll 1
   for (int i = tid; i < HS; i += NT) { hkey[i] = -1; hfirst[i] = 0; }
@@ -1036,11 +1045,13 @@ __device__ void phase2_scatter_atomic(const StepParams& p) {
   const float nlr = -p.lr;
   #pragma unroll 1
   for (int L = blockIdx.x; L < p.NLtot; L += gridDim.x) {
-    const int U = __ldcg(p.list_off + (size_t)L * (P + 1) + P);
+    const int U0 = __ldcg(p.list_off + (size_t)L * (P + 1));
+    const int U1 = __ldcg(p.list_off + (size_t)L * (P + 1) + P);
     #pragma unroll 1
-    for (int j = warp; j < U; j += NW) {
-      const int row = __ldcg(p.list_rows + (size_t)L * p.cap + j);
-      const float* src = p.list_vals + ((size_t)L * p.cap + j) * d;
+    for (int j = U0 + warp; j < U1; j += NW) {
+      const size_t ix = list_index(p, L, j);
+      const int row = __ldcg(p.list_rows + ix);
+      const float* src = p.list_vals + ix * d;
       float* dst = p.C + (size_t)row * d;
       if ((d & 3) == 0) {
         #pragma unroll 1
@@ -1065,8 +1076,13 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
   // ---- trip 1: everything that does not depend on the decision
   unsigned my_done = 0;
   if (tid == 0) {
-    const int f = __ldcg(&st->flags);
+    int f = __ldcg(&st->flags);
     const unsigned long long bad = __ldcg(&st->bad);
+    if (p.flags_from_records) {   // data parallel: every rank skips together
+      f = 0;
+      for (int r = 0; r < p.Ptot; ++r)
+        f |= __float_as_int(__ldcg(p.dense_part + (size_t)r * p.dense_stride + p.dense_len + 1));
+    }
     s_flags = f;
     if (blockIdx.x == 0) st->last_bad = bad;
     my_done = atomicAdd(&st->done, 1u);   // result consumed only at the end (flag reset)
@@ -1118,6 +1134,7 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
   if (blockIdx.x == 0 && tid == 0) {
     st->last_loss = loss;
     st->last_flags = flags;
+    st->rank_flags = flags;
     if (p.loss_out) *p.loss_out = loss;
     if (flags) {
       atomicOr(&st->sticky_flags, flags);
@@ -1157,6 +1174,52 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
   }
 }
 
+// ------------------------------------------------------------------ data-parallel record
+// After phase 1 (and the in-rank grid barrier): this rank's compact record for
+// the all-gather -- the dense partials summed in CTA order, the hinge sum and
+// flags, and every list's entries compacted into one array with absolute
+// per-owner offsets.
+__device__ void build_record(const StepParams& p, unsigned char* sm) {
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  const int P = p.P, d = p.d, NL = p.NLtot;
+  int* ws = reinterpret_cast<int*>(sm + p.lay.ws2);
+  // dense sums: this CTA's quad slice over the P partials
+  const DenseSlice ds = dense_slice(p);
+#pragma unroll 1
+  for (int qb = ds.q0; qb < ds.q1; qb += NT) {
+    const int nq = min(NT, ds.q1 - qb), groups = dense_groups(nq, NT);
+    dense_apply(p, sm, qb, nq, groups, dense_partial(p, qb, nq, groups), make_float4(0.f, 0.f, 0.f, 0.f), false,
+                p.send_dense);
+  }
+  if (blockIdx.x == 0 && warp == 0) {
+    float acc = 0.f;
+    for (int r = lane; r < P; r += 32) acc += __ldcg(p.dense_part + (size_t)r * p.dense_stride + p.dense_len);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      p.send_dense[p.dense_len] = acc;
+      p.send_dense[p.dense_len + 1] = __int_as_float(__ldcg(&p.st->flags));
+    }
+  }
+  // compaction: CTA b copies its lists L = b*R + r to [base_L, base_L + U_L)
+  __shared__ int s_base;
+#pragma unroll 1
+  for (int r = 0; r < p.R; ++r) {
+    const int L = blockIdx.x * p.R + r;
+    int part = 0;
+    for (int l = tid; l < L; l += NT) part += __ldcg(p.list_off + (size_t)l * (P + 1) + P);
+    int base;
+    block_excl_scan(part, ws, &base);   // total over lists < L
+    const int32_t* off = p.list_off + (size_t)L * (P + 1);
+    const int U = __ldcg(off + P);
+    for (int q = tid; q <= P; q += NT) p.send_off[(size_t)L * (P + 1) + q] = base + __ldcg(off + q);
+    const int32_t* lrows = p.list_rows + (size_t)L * p.list_stride;
+    const float* lvals = p.list_vals + (size_t)L * p.list_stride * d;
+    for (int j = tid; j < U; j += NT) p.send_rows[base + j] = __ldcg(lrows + j);
+    for (int t = tid; t < U * d; t += NT) p.send_vals[(size_t)base * d + t] = __ldcg(lvals + t);
+    (void)s_base; (void)NW; (void)NL;
+  }
+}
+
 // ------------------------------------------------------------------ kernels
 template <bool FAST>
 __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) {
@@ -1178,8 +1241,9 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
     __syncthreads();
     trace_mark(p, 6);
   }
-  if (phases == 3) grid_barrier(&p.st->bar_count, &p.st->bar_gen, my_gen);
+  if ((phases & 1) && (phases & 6)) grid_barrier(&p.st->bar_count, &p.st->bar_gen, my_gen);
   trace_mark(p, 7);
+  if (phases & 4) build_record(p, smem);
   if (phases & 2) phase2(p, smem);
   __syncthreads();
   trace_mark(p, 11);
@@ -1214,6 +1278,15 @@ cudaError_t step_prepare(int fast, size_t optin, size_t* usable) {
   const size_t smem = optin - fa.sharedSizeBytes;
   if (usable) *usable = smem;
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+void launch_step_phases(const StepParams& p, int phases, int fast, cudaStream_t s, int* launches) {
+  const int NT = step_block_threads(p.d, p.n, p.h, fast);
+  void* fn = fast ? (void*)step_kernel<true> : (void*)step_kernel<false>;
+  void* args[] = {(void*)&p, (void*)&phases};
+  if ((phases & 1) && (phases & 6)) cudaLaunchCooperativeKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
+  else cudaLaunchKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
+  *launches += 1;
 }
 
 void launch_step(const StepParams& p, int fused, int fast, cudaStream_t s, int* launches) {

@@ -117,7 +117,7 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   if (SB < 16) SB = 16;
   L.SB = SB;
   L.stagefb = o; o = align16(o + SB * d * 4);
-  L.carry = o; o = align16(o + d * 4);
+  L.carry = o; o = align16(o + 2 * d * 4);
   L.total2 = o > fast_end ? o : fast_end;
   return L;
 }
@@ -153,6 +153,18 @@ struct StepParams {
   // phase 2 sees Ptot records / NLtot lists (== P / P*R on one GPU;
   // world*P / world*P*R after a data-parallel all-gather)
   int Ptot, NLtot;
+  // list addressing: entry `off` of list L lives at index
+  //   (L / LPR) * rank_stride + (L % LPR) * list_stride + off
+  // single GPU: LPR = NLtot, list_stride = cap; after a data-parallel gather
+  // of compacted per-rank lists: LPR = lists per rank, list_stride = 0,
+  // rank_stride = entries per rank record (offsets are absolute in the record)
+  int LPR, list_stride, rank_stride;
+  int flags_from_records;   // phase 2 ORs the ranks' flags (dense record word dense_len+1)
+  // data-parallel record build (phase bit 4): this rank's compact record
+  float* send_dense;    // [dense_stride]: dense sums | hinge | flags
+  int32_t* send_off;    // [NL][P+1] absolute offsets into send_rows
+  int32_t* send_rows;   // [rec_cap]
+  float* send_vals;     // [rec_cap][d]
   DevStatus* st;
   float* loss_out;      // optional device pointer
   int mode;             // 0 det, 1 atomic
@@ -162,6 +174,8 @@ struct StepParams {
 };
 
 void launch_step(const StepParams& p, int fused, int fast, cudaStream_t s, int* launches);
+// phases: 1 phase 1, 2 phase 2, 4 data-parallel record (1|4 and 1|2 add the grid barrier)
+void launch_step_phases(const StepParams& p, int phases, int fast, cudaStream_t s, int* launches);
 int step_fast_ok(int d, int n, int h);
 int step_block_threads(int d, int n, int h, int fast);
 int step_chunk_T(int d, int n, int h, int fast);

@@ -200,3 +200,23 @@ def test_large_shape_generic_path(pg):
     gl, rl, p0, pend, ref = run_both(m, V, d, n, h, B=512, steps=2)
     assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3)
     m.close()
+
+
+def test_owner_overflow_sorted_fallback(pg):
+    # every row id is a multiple of 148 -> all gradient rows belong to owner 0,
+    # whose entry count exceeds the hash fast path (sorted fallback, several windows)
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    B = 4096
+    rng = np.random.default_rng(0)
+    idx = (rng.integers(0, V // 148, size=(B, n)) * 148).astype(np.int32)
+    corr = (rng.integers(0, V // 148, size=B) * 148).astype(np.int32)
+    # saturated regime: embedding updates far above the fp32 storage floor
+    start = synth.random_params(V, d, n, h, seed=5, w1_scale=200 * 0.5 / (n * d), w2_scale=200 * 0.5 / h)
+    m = make(pg, POLY)
+    m.set_params(*start[:4], b2=start[4])
+    p0 = m.get_params()
+    ref = oracle_from_gpu_params(p0, V, d, n, h)
+    gl = [m.train_step(idx, corr, 0.1)]
+    rl = [oracle.train_step(ref, idx, corr, 0.1)]
+    assert_parity(np.array(gl), np.array(rl), p0, m.get_params(), ref, tau_delta=1e-4)
+    m.close()
