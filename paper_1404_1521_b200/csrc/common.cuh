@@ -38,28 +38,29 @@ __device__ __forceinline__ float4 ldcg4(const float* p) {
 }
 
 // ---------------------------------------------------------------- grid barrier
-// Sense-reversing barrier for a cooperative (co-resident) grid.  State lives in
-// device memory and survives across launches: `count` returns to 0 after every
-// barrier and `gen` increases monotonically.  `my_gen` must be read (relaxed)
-// before this CTA arrives -- e.g. at kernel start -- so the wait costs no extra
-// round trip.  Ordering: bar.sync makes the CTA's writes visible to thread 0;
-// the acq_rel arrival RMW (cumulative) and the release store of `gen` publish
-// them; waiters acquire `gen` and bar.sync again.
+// Barrier for a cooperative (co-resident) grid on a monotonic 64-bit arrival
+// counter that is never reset: every instance adds exactly gridDim.x, so the
+// arrival value `old` names the instance (old / G) and its release point
+// ((old / G + 1) * G).  Waiters poll the counter itself -- one L2 round trip
+// after the last arrival, no separate generation word.  All users of one
+// counter must launch the same grid size.  Ordering: bar.sync makes the CTA's
+// writes visible to thread 0; its acq_rel arrival RMW (cumulative) publishes
+// them; the waiter's acquire load of the final count synchronises with every
+// arrival, and bar.sync hands that on to the CTA.
 __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned my_gen) {
+__device__ __forceinline__ void grid_barrier(unsigned long long* arrivals) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned arrived = atom_add_acqrel_gpu(count, 1u);
-    if (arrived == gridDim.x - 1) {
-      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(count), "r"(0u) : "memory");
-      st_release_gpu(gen, my_gen + 1);
-    } else {
-      while (ld_acquire_gpu(gen) == my_gen) {
-      }
+    unsigned long long old;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(arrivals) : "memory");
+    const unsigned long long G = gridDim.x, target = (old / G + 1) * G;
+    unsigned long long now = old + 1;
+    while (now < target) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(now) : "l"(arrivals) : "memory");
     }
   }
   __syncthreads();

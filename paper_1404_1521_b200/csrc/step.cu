@@ -83,27 +83,33 @@ __device__ __forceinline__ void agg_reset(const StepParams& p, unsigned char* sm
   #pragma unroll 1
   for (int i = threadIdx.x; i < 256; i += blockDim.x) { ocnt[i] = 0; ocur[i] = 0; ecur[i] = 0; }
   if (threadIdx.x == 0) misc[0] = 0;
+  uint4* am = reinterpret_cast<uint4*>(sm + lay.amask);
+  #pragma unroll 1
+  for (int i = threadIdx.x; i < 2 * kMaxKeys * (kMaxKeys / 32) / 4; i += blockDim.x) am[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
-// Stable counting sort of items 0..n-1 into buckets bucket[i], given the
-// buckets' exclusive offsets off[]: writes out[off[b] + rank] = i where rank =
-// #{i' < i : bucket[i'] == b}.  Block-parallel O(n^2 / threads) broadcast
-// scan -- no match_any (slow on this part) and no serial warp.
-__device__ __forceinline__ void stable_place(int n, const int* bucket, const int* off, unsigned short* out) {
-  #pragma unroll 1
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int b = bucket[i];
-    int r = 0;
-    int j = 0;
-    #pragma unroll 1
-    for (; j + 4 <= i; j += 4) {
-      const int4 q = *reinterpret_cast<const int4*>(bucket + j);
-      r += (q.x == b) + (q.y == b) + (q.z == b) + (q.w == b);
+// Stable rank of item i inside its bucket: the number of the bucket's members
+// below i, read off the bucket's membership bitmask (bit i set for member i;
+// NWORDS 32-bit words, built with atomicOr, so the result does not depend on
+// the order in which members were discovered).  O(NWORDS) per item.
+template <int NWORDS>
+__device__ __forceinline__ int mask_rank(const unsigned* mask, int i) {
+  const int wi = i >> 5;
+  int r = 0;
+#pragma unroll
+  for (int w4 = 0; w4 < NWORDS / 4; ++w4) {
+    if (4 * w4 <= wi) {
+      const uint4 m4 = reinterpret_cast<const uint4*>(mask)[w4];
+      const unsigned mw[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int w = 4 * w4 + k;
+        const unsigned keep = w < wi ? ~0u : (w == wi ? (1u << (i & 31)) - 1u : 0u);
+        r += __popc(mw[k] & keep);
+      }
     }
-    #pragma unroll 1
-    for (; j < i; ++j) r += bucket[j] == b;
-    out[off[b] + r] = (unsigned short)i;
   }
+  return r;
 }
 
 // Ordered sum of the rows src[pos[0..m)] (row stride d) for the features
@@ -141,6 +147,31 @@ __device__ __forceinline__ float4 ordered_rowsum(const float* src, const unsigne
                      (a[0][2] + a[1][2]) + (a[2][2] + a[3][2]), (a[0][3] + a[1][3]) + (a[2][3] + a[3][3]));
 }
 
+// The same ordered sum for one float4 of the features (q = feature quad) --
+// thread-granular, so many (row, quad) items run in parallel.  Identical
+// association: chains c = i mod 4, combined (a0 + a1) + (a2 + a3).
+__device__ __forceinline__ float4 ordered_quadsum(const float4* src, const unsigned short* pos, int m, int Q, int q) {
+  float4 a[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) a[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+  for (int i = 0; i < m; i += 4) {
+    float4 v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = src[(size_t)pos[i + c < m ? i + c : i] * Q + q];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const bool ok = i + c < m;
+      a[c].x += ok ? v[c].x : 0.f;
+      a[c].y += ok ? v[c].y : 0.f;
+      a[c].z += ok ? v[c].z : 0.f;
+      a[c].w += ok ? v[c].w : 0.f;
+    }
+  }
+  return make_float4((a[0].x + a[1].x) + (a[2].x + a[3].x), (a[0].y + a[1].y) + (a[2].y + a[3].y),
+                     (a[0].z + a[1].z) + (a[2].z + a[3].z), (a[0].w + a[1].w) + (a[2].w + a[3].w));
+}
+
 __device__ void aggregate_chunk(const StepParams& p, int L, int K, const int* rows_s,
                                 const float* Gs, unsigned char* sm) {
   const Layout& lay = p.lay;
@@ -153,6 +184,7 @@ __device__ void aggregate_chunk(const StepParams& p, int L, int K, const int* ro
   int* hj = reinterpret_cast<int*>(sm + lay.hj);
   int* misc = reinterpret_cast<int*>(sm + lay.misc);
   int* ws = reinterpret_cast<int*>(sm + lay.ws);
+  unsigned* amask = reinterpret_cast<unsigned*>(sm + lay.amask);
   const int P = p.P, d = p.d, HA = 2 * kMaxKeys;
   // pass 1: insert + multiplicity; the inserting thread counts the row for its owner
   bool creator = false;
@@ -171,6 +203,7 @@ __device__ void aggregate_chunk(const StepParams& p, int L, int K, const int* ro
     }
     hslot[i] = (int)h;
     atomicAdd(&hc[h], 1);
+    atomicOr(&amask[h * (kMaxKeys / 32) + (i >> 5)], 1u << (i & 31));
     if (mine) { creator = true; my_row = row; my_h = h; atomicAdd(&ocnt[(unsigned)row % (unsigned)P], 1); }
   }
   __syncthreads();
@@ -200,8 +233,6 @@ __device__ void aggregate_chunk(const StepParams& p, int L, int K, const int* ro
     ecnt[j] = hc[my_h];
   }
   __syncthreads();
-  #pragma unroll 1
-  for (int i = tid; i < K; i += NT) hslot[i] = hj[hslot[i]];   // position -> entry
   {
     const int v = tid < nU ? ecnt[tid] : 0;
     int tot;
@@ -210,38 +241,39 @@ __device__ void aggregate_chunk(const StepParams& p, int L, int K, const int* ro
   }
   __syncthreads();
   if (tr) trace_mark(p, 16);
-  // pass 3: positions grouped by entry, increasing within each entry (one warp)
-  stable_place(K, hslot, eoff, spos);
+  // pass 3: positions grouped by entry, increasing within each entry
+  #pragma unroll 1
+  for (int i = tid; i < K; i += NT) {
+    const int h = hslot[i];
+    spos[eoff[hj[h]] + mask_rank<kMaxKeys / 32>(amask + h * (kMaxKeys / 32), i)] = (unsigned short)i;
+  }
   __syncthreads();
   if (tr) trace_mark(p, 18);
-  // pass 4: warp per entry -- ordered sum of its gradient rows, one coalesced store
+  // pass 4: ordered sum of each entry's gradient rows, one thread per (entry, quad)
   float* lvals = p.list_vals + (size_t)L * p.cap * d;
-  #pragma unroll 1
-  long long t_sum = 0, t_st = 0;
-  int n_ent = 0;
+  if ((d & 3) == 0) {
+    const int Q = d >> 2;
+    const float4* G4 = reinterpret_cast<const float4*>(Gs);
 #pragma unroll 1
-  for (int j = warp; j < nU; j += NW) {
-    const int m = ecnt[j];
-    const unsigned short* ps = spos + eoff[j];
-    float* dst = lvals + (size_t)j * d;
-#pragma unroll 1
-    for (int f0 = 0; f0 < d; f0 += 128) {
-      const long long c0 = clock64();
-      const float4 o4 = ordered_rowsum(Gs, ps, m, d, f0);
-      const float out[4] = {o4.x, o4.y, o4.z, o4.w};
-      const long long c1 = clock64();
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        if (f0 + lane + 32 * kk < d) dst[f0 + lane + 32 * kk] = out[kk];
-      t_sum += c1 - c0;
-      t_st += clock64() - c1;
-      ++n_ent;
+    for (int it = tid; it < nU * Q; it += NT) {
+      const int j = it / Q, q = it - j * Q;
+      reinterpret_cast<float4*>(lvals + (size_t)j * d)[q] = ordered_quadsum(G4, spos + eoff[j], ecnt[j], Q, q);
     }
-  }
-  if (tr && p.trace != nullptr && lane == 0 && blockIdx.x < 4 && warp < 4) {
-    p.trace[blockIdx.x * 32 + 20 + warp * 3 + 0] = t_sum;
-    p.trace[blockIdx.x * 32 + 20 + warp * 3 + 1] = t_st;
-    p.trace[blockIdx.x * 32 + 20 + warp * 3 + 2] = n_ent;
+  } else {
+#pragma unroll 1
+    for (int j = warp; j < nU; j += NW) {
+      const int m = ecnt[j];
+      const unsigned short* ps = spos + eoff[j];
+      float* dst = lvals + (size_t)j * d;
+#pragma unroll 1
+      for (int f0 = 0; f0 < d; f0 += 128) {
+        const float4 o4 = ordered_rowsum(Gs, ps, m, d, f0);
+        const float out[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          if (f0 + lane + 32 * kk < d) dst[f0 + lane + 32 * kk] = out[kk];
+      }
+    }
   }
   if (tr) trace_mark(p, 17);
   __syncthreads();
@@ -925,6 +957,9 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
   }
   #pragma unroll 1
   for (int i = tid; i < HS; i += NT) { hkey[i] = -1; hfirst[i] = 0; }
+  unsigned* rmask = reinterpret_cast<unsigned*>(sm + lay.rmask);
+  #pragma unroll 1
+  for (int i = tid; i < lay.MCAP * 4; i += NT) reinterpret_cast<uint4*>(rmask)[i] = make_uint4(0u, 0u, 0u, 0u);
   if (tid == 0) reinterpret_cast<int*>(sm + lay.rcur)[lay.MCAP] = 0;
   __syncthreads();
   // ---- trip 2: row ids and gradient partials of all entries at once (TMA bulk copies)
@@ -984,7 +1019,11 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
   if (my_r[0] >= 0) rcnt[my_r[0]] = hcnt[my_hs[0]];
   if (my_r[1] >= 0) rcnt[my_r[1]] = hcnt[my_hs[1]];
   #pragma unroll 1
-  for (int e = tid; e < M; e += NT) eslot[e] = hrid[eslot[e]];   // entry -> distinct row
+  for (int e = tid; e < M; e += NT) {   // entry -> distinct row; row membership mask
+    const int r = hrid[eslot[e]];
+    eslot[e] = r;
+    atomicOr(&rmask[r * 16 + (e >> 5)], 1u << (e & 31));
+  }
   __syncthreads();
   {
     int running = 0;
@@ -999,8 +1038,12 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
     }
   }
   __syncthreads();
-  // entries grouped by row, in list order within each row (one warp)
-  stable_place(M, eslot, roff, hlist);
+  // entries grouped by row, in list order within each row
+  #pragma unroll 1
+  for (int e = tid; e < M; e += NT) {
+    const int r = eslot[e];
+    hlist[roff[r] + mask_rank<16>(rmask + r * 16, e)] = (unsigned short)e;
+  }
   // ---- trip 3: C rows of the first 4*NW distinct rows, bulk-copied while the
   // staged partials are still in flight
   float* cstage = reinterpret_cast<float*>(sm + lay.cstage);
@@ -1015,22 +1058,38 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
   else asm volatile("cp.async.wait_group 0;" ::: "memory");
   if (ncp > 0) mbar_wait(cbar, 0);
   __syncthreads();
-  // ---- warp per distinct row: ordered sum of its partials, one RMW of C
+  // ---- ordered sum of each distinct row's partials, one RMW of C; one thread
+  // per (row, feature quad) when d % 4 == 0, else one warp per row
+  if ((d & 3) == 0) {
+    const int Q = d >> 2;
+    const float4* S4 = reinterpret_cast<const float4*>(stage);
 #pragma unroll 1
-  for (int ri = warp; ri < nrows; ri += NW) {
-    float* crow = p.C + (size_t)rrow[ri] * d;
-    const float* cold = ri < ncp ? cstage + (size_t)ri * d : nullptr;
-    const int nm = rcnt[ri];
-    const unsigned short* ps = hlist + roff[ri];
-#pragma unroll 1
-    for (int f0 = 0; f0 < d; f0 += 128) {
-      const float4 a4 = ordered_rowsum(stage, ps, nm, d, f0);
-      const float acc[4] = {a4.x, a4.y, a4.z, a4.w};
+    for (int it = tid; it < nrows * Q; it += NT) {
+      const int ri = it / Q, q = it - ri * Q;
+      const float4 a = ordered_quadsum(S4, hlist + roff[ri], rcnt[ri], Q, q);
       if (write) {
+        float4* c4 = reinterpret_cast<float4*>(p.C + (size_t)rrow[ri] * d) + q;
+        const float4 o = ri < ncp ? reinterpret_cast<const float4*>(cstage + (size_t)ri * d)[q] : __ldcg(c4);
+        *c4 = make_float4(o.x + nlr * a.x, o.y + nlr * a.y, o.z + nlr * a.z, o.w + nlr * a.w);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int ri = warp; ri < nrows; ri += NW) {
+      float* crow = p.C + (size_t)rrow[ri] * d;
+      const float* cold = ri < ncp ? cstage + (size_t)ri * d : nullptr;
+      const int nm = rcnt[ri];
+      const unsigned short* ps = hlist + roff[ri];
+#pragma unroll 1
+      for (int f0 = 0; f0 < d; f0 += 128) {
+        const float4 a4 = ordered_rowsum(stage, ps, nm, d, f0);
+        const float acc[4] = {a4.x, a4.y, a4.z, a4.w};
+        if (write) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int f = f0 + lane + 32 * k;
-          if (f < d) crow[f] = (cold ? cold[f] : __ldcg(crow + f)) + nlr * acc[k];
+          for (int k = 0; k < 4; ++k) {
+            const int f = f0 + lane + 32 * k;
+            if (f < d) crow[f] = (cold ? cold[f] : __ldcg(crow + f)) + nlr * acc[k];
+          }
         }
       }
     }
@@ -1224,7 +1283,6 @@ __device__ void build_record(const StepParams& p, unsigned char* sm) {
 template <bool FAST>
 __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const unsigned my_gen = ld_relaxed_gpu(&p.st->bar_gen);   // consumed at the grid barrier
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + p.lay.mbar);
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
@@ -1241,7 +1299,7 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
     __syncthreads();
     trace_mark(p, 6);
   }
-  if ((phases & 1) && (phases & 6)) grid_barrier(&p.st->bar_count, &p.st->bar_gen, my_gen);
+  if ((phases & 1) && (phases & 6)) grid_barrier(&p.st->bar_arrivals);
   trace_mark(p, 7);
   if (phases & 4) build_record(p, smem);
   if (phases & 2) phase2(p, smem);

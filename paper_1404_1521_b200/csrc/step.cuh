@@ -15,8 +15,7 @@ struct DevStatus {
   unsigned long long last_bad;   // result of the most recent step
   unsigned long long sticky_bad; // min over asynchronous steps since pg_sync
   unsigned long long score_bad;  // pg_score index check
-  unsigned bar_count;            // grid barrier arrivals (returns to 0)
-  unsigned bar_gen;              // grid barrier generation
+  unsigned long long bar_arrivals; // grid barrier: monotonic arrival count (never reset)
   unsigned done;                 // phase-2 arrival counter (flag-reset protocol)
   int flags;                     // current step: bit0 bad index
   int last_flags;                // most recent step: bit0 bad index, bit1 non-finite loss
@@ -31,11 +30,11 @@ struct DevStatus {
 struct Layout {
   // phase 1
   int xs, pg, sig, gz, hinge, rows, ws, red, wsm, mbar;
-  int ahk, ahc, aslot, ocnt, ocur, hj, ecnt, eoff, ecur, spos, misc;   // chunk aggregation
+  int ahk, ahc, aslot, ocnt, ocur, hj, ecnt, eoff, ecur, spos, misc, amask;   // chunk aggregation
   int A, Ac, SIG, DEL, DELc;   // generic path
   // phase 2
   int lbase, loff, keys, seg, stage, stagefb, carry, dred, ws2;
-  int esrc, erow, hkey, hfirst, heads, hlist, rcnt, roff, rcur, misc2, cstage;
+  int esrc, erow, hkey, hfirst, heads, hlist, rcnt, roff, rcur, misc2, cstage, rmask;
   int SB;        // staged rows per sub-batch (sorted fallback)
   int MCAP;      // owner entries handled by the hash fast path
   int HS;        // hash slots (power of two >= 2*MCAP)
@@ -78,6 +77,7 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.ecur = o;  o = align16(o + kMaxKeys * 4);
   L.spos = o;  o = align16(o + kMaxKeys * 2);
   L.misc = o;  o = align16(o + 16 * 4);
+  L.amask = o; o = align16(o + 2 * kMaxKeys * (kMaxKeys / 32) * 4);   // per hash slot: member positions
   L.ws = o;    o = align16(o + 64 * 4);
   L.red = o;   o = align16(o + 2 * 32 * 32 * 4);
   L.total1 = o;
@@ -107,6 +107,7 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.hfirst = o; o = align16(o + HS * 4);
   L.stage = o;  o = align16(o + MCAP * d * 4);
   L.cstage = o; o = align16(o + 4 * NW * d * 4);     // C rows of each warp's first 4 distinct rows
+  L.rmask = o;  o = align16(o + MCAP * (512 / 32) * 4);   // per distinct row: member entries
   const int fast_end = o;
   // sorted fallback (aliases the hash path)
   o = p2fixed;
