@@ -82,7 +82,7 @@ __device__ __forceinline__ void agg_reset(const StepParams& p, unsigned char* sm
   int* ecur = reinterpret_cast<int*>(sm + lay.ecur);
   #pragma unroll 1
   for (int i = threadIdx.x; i < 256; i += blockDim.x) { ocnt[i] = 0; ocur[i] = 0; ecur[i] = 0; }
-  if (threadIdx.x == 0) misc[0] = 0;
+  if (threadIdx.x == 0) { misc[0] = 0; misc[1] = 0; }
   uint4* am = reinterpret_cast<uint4*>(sm + lay.amask);
   #pragma unroll 1
   for (int i = threadIdx.x; i < 2 * kMaxKeys * (kMaxKeys / 32) / 4; i += blockDim.x) am[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -172,24 +172,23 @@ __device__ __forceinline__ float4 ordered_quadsum(const float4* src, const unsig
                      (a[0].z + a[1].z) + (a[2].z + a[3].z), (a[0].w + a[1].w) + (a[2].w + a[3].w));
 }
 
-__device__ void aggregate_chunk(const StepParams& p, int L, int K, const int* rows_s,
-                                const float* Gs, unsigned char* sm) {
+// Aggregation pass 1 (run as soon as the chunk's row ids are known): insert the
+// K row ids into the smem hash (slot per position, multiplicity, membership
+// bitmask), count each distinct row for its owner, and number the distinct rows
+// u = 0..nU-1 (urow / uslot; the numbering order is arbitrary and only decides
+// where a row is staged).  Ends with a barrier; returns nU.
+__device__ int agg_insert(const StepParams& p, int K, const int* rows_s, unsigned char* sm) {
   const Layout& lay = p.lay;
-  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  const int tid = threadIdx.x, NT = blockDim.x;
   int* hk = reinterpret_cast<int*>(sm + lay.ahk);
   int* hc = reinterpret_cast<int*>(sm + lay.ahc);
   int* hslot = reinterpret_cast<int*>(sm + lay.aslot);
   int* ocnt = reinterpret_cast<int*>(sm + lay.ocnt);
-  int* ocur = reinterpret_cast<int*>(sm + lay.ocur);
-  int* hj = reinterpret_cast<int*>(sm + lay.hj);
   int* misc = reinterpret_cast<int*>(sm + lay.misc);
-  int* ws = reinterpret_cast<int*>(sm + lay.ws);
+  int* urow = reinterpret_cast<int*>(sm + lay.urow);
+  int* uslot = reinterpret_cast<int*>(sm + lay.uslot);
   unsigned* amask = reinterpret_cast<unsigned*>(sm + lay.amask);
-  const int P = p.P, d = p.d, HA = 2 * kMaxKeys;
-  // pass 1: insert + multiplicity; the inserting thread counts the row for its owner
-  bool creator = false;
-  int my_row = 0;
-  unsigned my_h = 0;
+  const int P = p.P, HA = 2 * kMaxKeys;
   #pragma unroll 1
   for (int i = tid; i < K; i += NT) {
     const int row = rows_s[i];
@@ -204,9 +203,33 @@ __device__ void aggregate_chunk(const StepParams& p, int L, int K, const int* ro
     hslot[i] = (int)h;
     atomicAdd(&hc[h], 1);
     atomicOr(&amask[h * (kMaxKeys / 32) + (i >> 5)], 1u << (i & 31));
-    if (mine) { creator = true; my_row = row; my_h = h; atomicAdd(&ocnt[(unsigned)row % (unsigned)P], 1); }
+    if (mine) {
+      atomicAdd(&ocnt[(unsigned)row % (unsigned)P], 1);
+      const int u = atomicAdd(&misc[1], 1);
+      urow[u] = row;
+      uslot[u] = (int)h;
+    }
   }
   __syncthreads();
+  return misc[1];
+}
+
+__device__ void aggregate_chunk(const StepParams& p, int L, int K, const int* rows_s,
+                                const float* Gs, unsigned char* sm) {
+  const Layout& lay = p.lay;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  int* hc = reinterpret_cast<int*>(sm + lay.ahc);
+  int* hslot = reinterpret_cast<int*>(sm + lay.aslot);
+  int* ocnt = reinterpret_cast<int*>(sm + lay.ocnt);
+  int* ocur = reinterpret_cast<int*>(sm + lay.ocur);
+  int* hj = reinterpret_cast<int*>(sm + lay.hj);
+  int* misc = reinterpret_cast<int*>(sm + lay.misc);
+  int* ws = reinterpret_cast<int*>(sm + lay.ws);
+  const int* urow = reinterpret_cast<const int*>(sm + lay.urow);
+  const int* uslot = reinterpret_cast<const int*>(sm + lay.uslot);
+  unsigned* amask = reinterpret_cast<unsigned*>(sm + lay.amask);
+  const int P = p.P, d = p.d;
+  const int nUd = misc[1];   // distinct rows (agg_insert)
   const bool tr = (L % p.R) == 0;
   if (tr) trace_mark(p, 14);
   int32_t* off = p.list_off + (size_t)L * (P + 1);
@@ -225,12 +248,14 @@ __device__ void aggregate_chunk(const StepParams& p, int L, int K, const int* ro
   int* eoff = reinterpret_cast<int*>(sm + lay.eoff);
   int* ecur = reinterpret_cast<int*>(sm + lay.ecur);
   unsigned short* spos = reinterpret_cast<unsigned short*>(sm + lay.spos);
-  if (creator) {
-    const int q = (int)((unsigned)my_row % (unsigned)P);
+  #pragma unroll 1
+  for (int u = tid; u < nUd; u += NT) {
+    const int row = urow[u], h = uslot[u];
+    const int q = (int)((unsigned)row % (unsigned)P);
     const int j = ocnt[q] + atomicAdd(&ocur[q], 1);
-    hj[my_h] = j;
-    lrows[j] = my_row;
-    ecnt[j] = hc[my_h];
+    hj[h] = j;
+    lrows[j] = row;
+    ecnt[j] = hc[h];
   }
   __syncthreads();
   {
@@ -291,41 +316,57 @@ __device__ void write_empty_list(const StepParams& p, int L) {
 // input [x_0 .. x_{n-1}, x'_c]; its W1 rows live in registers for the whole
 // step (Wcol for the forward, Wrow for the gradient rows).
 
-// Gather the chunk's K = cnt*(n+1) embedding rows into X[e][slot][0..d) with one
-// bulk copy (TMA engine) per valid row, completing on `bar`.  With `wblock`,
-// also stage every warp's 32 W1 rows (128 B each) into its padded smem block.
-// Returns the parity to wait on.
-__device__ __forceinline__ void gather_rows_bulk(const StepParams& p, long long e0, int cnt, float* X,
-                                                 int* rows_s, unsigned long long* bar, float* wsm, bool wblock) {
-  const int tid = threadIdx.x, n = p.n, d = p.d, K = cnt * (n + 1);
-  int row = -1;
-  bool ok = false;
-  if (tid < K) {
-    const int e = tid / (n + 1), s = tid - e * (n + 1);
-    const long long ex = e0 + e;
+// Gather the chunk's K = cnt*(n+1) embedding rows.  The index loads are issued
+// first (the aggregation reset overlaps them); the row ids go through the
+// aggregation hash at once (agg_insert), and only the nU DISTINCT rows are
+// copied, to X[u][0..d), with pu[position] = u.  Deduplicating matters under
+// Zipf traffic: without it every CTA fetches the hot rows many times and the
+// requests pile up on the L2 slices holding them.  16 B cp.async pieces over all
+// threads (lower latency than one bulk copy per row; scripts/micro/gather_bench.cu).
+// Out-of-range indices are reported and read row 0 (the step is skipped).
+template <typename WLoad, typename WPost>
+__device__ __forceinline__ void gather_rows(const StepParams& p, unsigned char* sm, long long e0, int cnt,
+                                            float* X, int* rows_s, bool tr, WLoad&& wload, WPost&& wpost) {
+  const int tid = threadIdx.x, NT = blockDim.x, n = p.n, d = p.d, K = cnt * (n + 1);
+  int row = 0, s = 0;
+  long long ex = 0;
+  if (tid < K) {   // K <= blockDim.x (step_fast_ok)
+    const int e = tid / (n + 1);
+    s = tid - e * (n + 1);
+    ex = e0 + e;
     row = s < n ? __ldg(p.idx + ex * n + s) : __ldg(p.corr + ex);
-    ok = row >= 0 && (long long)row < p.V;
+  }
+  wload();   // caller's register loads, queued behind the index loads
+  agg_reset(p, sm);
+  if (tid < K) {
+    const bool ok = row >= 0 && (long long)row < p.V;
     if (!ok) report_bad(p.st, s < n ? ex * n + s : (long long)p.B * n + ex, row);
     rows_s[tid] = ok ? row : 0;
   }
-  const int nvalid = __syncthreads_count(ok);   // also orders prior generic smem use
-  if (e0 == (long long)blockIdx.x * p.B / p.P) trace_mark(p, 19);
-  const int NW = blockDim.x >> 5, DB = d >> 5, c = n >> 1;
-  const unsigned wbytes = (unsigned)(n * d * 32 * 4);   // all of W1 in one bulk copy
-  if (tid == 0) {
-    mbar_arrive_expect_tx(bar, (unsigned)(nvalid * d * 4) + (wblock ? wbytes : 0u));
-    fence_proxy_async();
-    if (wblock) bulk_g2s(wsm, p.W1, wbytes, bar);
+  __syncthreads();
+  if (tr) trace_mark(p, 19);
+  const int nU = agg_insert(p, K, rows_s, sm);
+  const Layout& lay = p.lay;
+  const int* urow = reinterpret_cast<const int*>(sm + lay.urow);
+  const int Q = d >> 2;
+  #pragma unroll 2
+  for (int it = tid; it < nU * Q; it += NT) {
+    const int u = it / Q, q = it - u * Q;
+    cp_async16(X + (size_t)u * d + 4 * q, p.C + (size_t)urow[u] * d + 4 * q);
   }
-  if (ok) {
-    fence_proxy_async();
-    bulk_g2s(X + (size_t)tid * d, p.C + (size_t)row * d, (unsigned)(d * 4), bar);
-  } else if (tid < K) {
-    #pragma unroll 1
-    for (int f = 0; f < d; ++f) X[(size_t)tid * d + f] = 0.f;
+  {   // position -> distinct index (slot -> u inverse of uslot)
+    int* pu = reinterpret_cast<int*>(sm + lay.pu);
+    int* hu = reinterpret_cast<int*>(sm + lay.hj);   // hash slot -> u (hj is rebuilt by the aggregation)
+    const int* uslot = reinterpret_cast<const int*>(sm + lay.uslot);
+    const int* hslot = reinterpret_cast<const int*>(sm + lay.aslot);
+    if (tid < nU) hu[uslot[tid]] = tid;
+    __syncthreads();
+    if (tid < K) pu[tid] = hu[hslot[tid]];
   }
-  (void)NW; (void)DB; (void)c;
-  if (nvalid < K) __syncthreads();   // zero-filled rows (bad index) visible to all warps
+  wpost();   // caller's work that only needs its own loads, while the rows land
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  if (tr) trace_mark(p, 25);
 }
 
 __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
@@ -336,17 +377,15 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
   const int wslot = slot == n ? c : slot;
   const int wrow0 = wslot * d + blk * 32;
   const int sel = slot == n ? 2 : (slot == c ? 1 : 0);  // sigma / delta / delta'
-  const int xstride = (n + 1) * d;                      // floats between examples in X
   float* X = reinterpret_cast<float*>(sm + lay.xs);
   float* pg = reinterpret_cast<float*>(sm + lay.pg);
   float* sig = reinterpret_cast<float*>(sm + lay.sig);
   float* hinge_s = reinterpret_cast<float*>(sm + lay.hinge);
   int* rows_s = reinterpret_cast<int*>(sm + lay.rows);
   float* red = reinterpret_cast<float*>(sm + lay.red);
-  float* wsm = reinterpret_cast<float*>(sm + lay.wsm);
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + lay.mbar);
-  const float* xw = X + slot * d + blk * 32;            // this warp's block of example 0
-  const float* wb = wsm + (size_t)wrow0 * 32;           // this warp's 32 W1 rows (unpadded)
+  const int* pu = reinterpret_cast<const int*>(sm + lay.pu);
+  // this warp's 32 features of example e's slot row (rows are deduplicated: pu)
+  auto xrow = [&](int e) -> const float* { return X + (size_t)pu[e * (n + 1) + slot] * d + blk * 32; };
 
   const long long lo = (long long)(((unsigned long long)blockIdx.x * (unsigned)p.B) / (unsigned)p.P);
   const long long hi = (long long)(((unsigned long long)(blockIdx.x + 1) * (unsigned)p.B) / (unsigned)p.P);
@@ -356,7 +395,6 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
   };
   const float b1 = __ldg(p.b1 + lane), w2 = __ldg(p.w2 + lane), b2 = __ldg(p.b2);
   float dacc[32];
-  unsigned parity = 0;
 #pragma unroll
   for (int u = 0; u < 32; ++u) dacc[u] = 0.f;
   float acc_db1 = 0.f, acc_dw2 = 0.f, acc_hinge = 0.f;
@@ -367,32 +405,34 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
     const int cnt = chunk_cnt(r);
     const int L = blockIdx.x * p.R + r;
     if (cnt <= 0) { write_empty_list(p, L); continue; }
-    agg_reset(p, sm);
-    gather_rows_bulk(p, e0, cnt, X, rows_s, bar, wsm, r == 0);
-    mbar_wait(bar, parity);
-    parity ^= 1;
-    // W1 block into registers for this chunk's forward / backward (re-read from
-    // smem every chunk so the registers are free during aggregation)
+    // This warp's W1 block straight into registers (L2-resident after the first
+    // CTA touches it), issued before the gather so its latency is hidden:
+    // Wcol[k] = W1[wrow0+k][lane] (forward), Wrow[u] = W1[wrow0+lane][u] (backward).
     float Wcol[32], Wrow[32];
+    float* wt = reinterpret_cast<float*>(sm + lay.wsm) + (size_t)warp * 32 * 33;
+    gather_rows(
+        p, sm, e0, cnt, X, rows_s, r == 0,
+        [&]() {   // coalesced: one 128 B W1 row per load
+          const float* wg = p.W1 + (size_t)wrow0 * 32;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) Wcol[k] = wb[k * 32 + lane];
-    {
-      const float4* wr = reinterpret_cast<const float4*>(wb + lane * 32);   // 8-way conflicts, once per chunk
+          for (int k = 0; k < 32; ++k) Wcol[k] = __ldg(wg + k * 32 + lane);
+        },
+        [&]() {   // Wrow = Wcol transposed across the warp, via a padded smem tile
 #pragma unroll
-      for (int u4 = 0; u4 < 8; ++u4) {
-        const float4 v = wr[u4];
-        Wrow[4 * u4] = v.x; Wrow[4 * u4 + 1] = v.y; Wrow[4 * u4 + 2] = v.z; Wrow[4 * u4 + 3] = v.w;
-      }
-    }
+          for (int k = 0; k < 32; ++k) wt[k * 33 + lane] = Wcol[k];
+          __syncwarp();
+#pragma unroll
+          for (int u = 0; u < 32; ++u) Wrow[u] = wt[lane * 33 + u];
+        });
     if (r == 0) trace_mark(p, 1);
     // ---- forward partials: part[warp][e][u] = sum_k x[e][k] W1[wrow0+k][u]
     float* part = pg;
     for (int e = 0; e < cnt; e += 4) {
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-      const float4* x0 = reinterpret_cast<const float4*>(xw + (size_t)(e + 0) * xstride);
-      const float4* x1 = reinterpret_cast<const float4*>(xw + (size_t)min(e + 1, cnt - 1) * xstride);
-      const float4* x2 = reinterpret_cast<const float4*>(xw + (size_t)min(e + 2, cnt - 1) * xstride);
-      const float4* x3 = reinterpret_cast<const float4*>(xw + (size_t)min(e + 3, cnt - 1) * xstride);
+      const float4* x0 = reinterpret_cast<const float4*>(xrow(e));
+      const float4* x1 = reinterpret_cast<const float4*>(xrow(min(e + 1, cnt - 1)));
+      const float4* x2 = reinterpret_cast<const float4*>(xrow(min(e + 2, cnt - 1)));
+      const float4* x3 = reinterpret_cast<const float4*>(xrow(min(e + 3, cnt - 1)));
 #pragma unroll
       for (int k4 = 0; k4 < 8; ++k4) {
         float4 v0 = x0[k4], v1 = x1[k4], v2 = x2[k4], v3 = x3[k4];
@@ -480,7 +520,7 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
     for (int e = 0; e < cnt; e += 2) {
       const bool two = e + 1 < cnt;
       const int e1 = two ? e + 1 : e;
-      const float xl0 = xw[(size_t)e * xstride + lane], xl1 = two ? xw[(size_t)e1 * xstride + lane] : 0.f;
+      const float xl0 = xrow(e)[lane], xl1 = two ? xrow(e1)[lane] : 0.f;
       const float4* sv0 = reinterpret_cast<const float4*>(sv_base + e * 32);
       const float4* sv1 = reinterpret_cast<const float4*>(sv_base + e1 * 32);
       float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, h0 = 0.f, h1 = 0.f, h2 = 0.f, h3 = 0.f;
@@ -676,6 +716,7 @@ __device__ void phase1_generic(const StepParams& p, unsigned char* sm) {
       Gs[i] = acc;
     }
     __syncthreads();
+    agg_insert(p, cnt * (n + 1), rows_s, sm);
     aggregate_chunk(p, L, cnt * (n + 1), rows_s, Gs, sm);
     first = false;
   }
@@ -955,6 +996,7 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
     }
     esrc[e] = (int)list_index(p, lo, loff[lo] + (e - lbase[lo]));
   }
+  trace_mark(p, 20);
   #pragma unroll 1
   for (int i = tid; i < HS; i += NT) { hkey[i] = -1; hfirst[i] = 0; }
   unsigned* rmask = reinterpret_cast<unsigned*>(sm + lay.rmask);
@@ -962,28 +1004,27 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
   for (int i = tid; i < lay.MCAP * 4; i += NT) reinterpret_cast<uint4*>(rmask)[i] = make_uint4(0u, 0u, 0u, 0u);
   if (tid == 0) reinterpret_cast<int*>(sm + lay.rcur)[lay.MCAP] = 0;
   __syncthreads();
-  // ---- trip 2: row ids and gradient partials of all entries at once (TMA bulk copies)
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + lay.mbar) + 1;
-  const bool bulk = (d & 3) == 0;
-  if (bulk) {
-    if (tid == 0) mbar_arrive_expect_tx(bar, (unsigned)(M * d * 4));
-    fence_proxy_async();
-    #pragma unroll 1
-    for (int e = tid; e < M; e += NT) {
-      erow[e] = __ldcg(p.list_rows + esrc[e]);
-      bulk_g2s(stage + (size_t)e * d, p.list_vals + (size_t)esrc[e] * d, (unsigned)(d * 4), bar);
+  // ---- trip 2: row ids and gradient partials of all entries at once (cp.async:
+  // lower latency than per-row bulk copies for these L2-resident records)
+  #pragma unroll 1
+  for (int e = tid; e < M; e += NT) erow[e] = __ldcg(p.list_rows + esrc[e]);
+  if ((d & 3) == 0) {
+    const int Q = d >> 2;
+    #pragma unroll 2
+    for (int it = tid; it < M * Q; it += NT) {
+      const int e = it / Q, q = it - e * Q;
+      cp_async16(stage + (size_t)e * d + 4 * q, p.list_vals + (size_t)esrc[e] * d + 4 * q);
     }
   } else {
-    #pragma unroll 1
-    for (int e = tid; e < M; e += NT) erow[e] = __ldcg(p.list_rows + esrc[e]);
     #pragma unroll 1
     for (int t = tid; t < M * d; t += NT) {
       const int e = t / d, f = t - e * d;
       cp_async4(stage + t, p.list_vals + (size_t)esrc[e] * d + f);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   __syncthreads();
+  trace_mark(p, 21);
   // ---- distinct rows: smem hash (row -> distinct index), multiplicity per row
   int* hcnt = hfirst;          // reused: per-slot multiplicity
   int* eslot = esrc;           // reused: entry -> hash slot (sources already issued)
@@ -1010,12 +1051,25 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
       const int r = atomicAdd(&rcur[lay.MCAP], 1);
       hrid[hsl] = r;
       rrow[r] = key;
-      my_r[k] = r;
-      my_hs[k] = (int)hsl;
+      if (k == 0) { my_r[0] = r; my_hs[0] = (int)hsl; }
+      else { my_r[1] = r; my_hs[1] = (int)hsl; }
     }
   }
   __syncthreads();
+  trace_mark(p, 22);
   const int nrows = rcur[lay.MCAP];
+  // trip 3, issued now: the C values of this thread's first (row, quad) items
+  const int Q = d >> 2;
+  const bool quad = (d & 3) == 0;
+  float4 cpre[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int it = tid + k * NT;
+    if (quad && it < nrows * Q) {
+      const int ri = it / Q, q = it - ri * Q;
+      cpre[k] = ldcg4(p.C + (size_t)rrow[ri] * d + 4 * q);
+    }
+  }
   if (my_r[0] >= 0) rcnt[my_r[0]] = hcnt[my_hs[0]];
   if (my_r[1] >= 0) rcnt[my_r[1]] = hcnt[my_hs[1]];
   #pragma unroll 1
@@ -1038,46 +1092,38 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
     }
   }
   __syncthreads();
+  trace_mark(p, 23);
   // entries grouped by row, in list order within each row
   #pragma unroll 1
   for (int e = tid; e < M; e += NT) {
     const int r = eslot[e];
     hlist[roff[r] + mask_rank<16>(rmask + r * 16, e)] = (unsigned short)e;
   }
-  // ---- trip 3: C rows of the first 4*NW distinct rows, bulk-copied while the
-  // staged partials are still in flight
-  float* cstage = reinterpret_cast<float*>(sm + lay.cstage);
-  unsigned long long* cbar = reinterpret_cast<unsigned long long*>(sm + lay.mbar) + 2;
-  const int ncp = bulk ? min(nrows, 4 * NW) : 0;
-  if (ncp > 0) {
-    if (tid == 0) mbar_arrive_expect_tx(cbar, (unsigned)(ncp * d * 4));
-    fence_proxy_async();
-    if (tid < ncp) bulk_g2s(cstage + (size_t)tid * d, p.C + (size_t)rrow[tid] * d, (unsigned)(d * 4), cbar);
-  }
-  if (bulk) mbar_wait(bar, 0);
-  else asm volatile("cp.async.wait_group 0;" ::: "memory");
-  if (ncp > 0) mbar_wait(cbar, 0);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
+  trace_mark(p, 24);
   // ---- ordered sum of each distinct row's partials, one RMW of C; one thread
   // per (row, feature quad) when d % 4 == 0, else one warp per row
-  if ((d & 3) == 0) {
-    const int Q = d >> 2;
+  if (quad) {
     const float4* S4 = reinterpret_cast<const float4*>(stage);
-#pragma unroll 1
-    for (int it = tid; it < nrows * Q; it += NT) {
+    auto item = [&](int it, bool pre, float4 o) {
       const int ri = it / Q, q = it - ri * Q;
       const float4 a = ordered_quadsum(S4, hlist + roff[ri], rcnt[ri], Q, q);
       if (write) {
         float4* c4 = reinterpret_cast<float4*>(p.C + (size_t)rrow[ri] * d) + q;
-        const float4 o = ri < ncp ? reinterpret_cast<const float4*>(cstage + (size_t)ri * d)[q] : __ldcg(c4);
+        if (!pre) o = __ldcg(c4);
         *c4 = make_float4(o.x + nlr * a.x, o.y + nlr * a.y, o.z + nlr * a.z, o.w + nlr * a.w);
       }
-    }
+    };
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (tid + k * NT < nrows * Q) item(tid + k * NT, true, cpre[k]);
+#pragma unroll 1
+    for (int it = tid + 4 * NT; it < nrows * Q; it += NT) item(it, false, make_float4(0.f, 0.f, 0.f, 0.f));
   } else {
 #pragma unroll 1
     for (int ri = warp; ri < nrows; ri += NW) {
       float* crow = p.C + (size_t)rrow[ri] * d;
-      const float* cold = ri < ncp ? cstage + (size_t)ri * d : nullptr;
       const int nm = rcnt[ri];
       const unsigned short* ps = hlist + roff[ri];
 #pragma unroll 1
@@ -1088,7 +1134,7 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const int f = f0 + lane + 32 * k;
-            if (f < d) crow[f] = (cold ? cold[f] : __ldcg(crow + f)) + nlr * acc[k];
+            if (f < d) crow[f] = __ldcg(crow + f) + nlr * acc[k];
           }
         }
       }
@@ -1179,7 +1225,7 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
     dacc0 = dense_partial(p, ds.q0, nq0, groups0);
     if (tid < nq0) {
       const int ndh = p.n * p.d * p.h, base = 4 * (ds.q0 + tid);
-#pragma unroll 1
+#pragma unroll
       for (int k = 0; k < 4; ++k)
         if (base + k < p.dense_len) cur0[k] = __ldcg(param_ptr(p, base + k, ndh));
     }

@@ -30,11 +30,11 @@ struct DevStatus {
 struct Layout {
   // phase 1
   int xs, pg, sig, gz, hinge, rows, ws, red, wsm, mbar;
-  int ahk, ahc, aslot, ocnt, ocur, hj, ecnt, eoff, ecur, spos, misc, amask;   // chunk aggregation
+  int ahk, ahc, aslot, ocnt, ocur, hj, ecnt, eoff, ecur, spos, misc, amask, pu, urow, uslot;   // chunk aggregation
   int A, Ac, SIG, DEL, DELc;   // generic path
   // phase 2
   int lbase, loff, keys, seg, stage, stagefb, carry, dred, ws2;
-  int esrc, erow, hkey, hfirst, heads, hlist, rcnt, roff, rcur, misc2, cstage, rmask;
+  int esrc, erow, hkey, hfirst, heads, hlist, rcnt, roff, rcur, misc2, rmask;
   int SB;        // staged rows per sub-batch (sorted fallback)
   int MCAP;      // owner entries handled by the hash fast path
   int HS;        // hash slots (power of two >= 2*MCAP)
@@ -53,7 +53,7 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
     L.pg = o;    o = align16(o + NW * T * 32 * 4);     // == T*(n+1)*d floats
     const int sigf = 3 * T * 32 > (d / 32) * 32 * 33 ? 3 * T * 32 : (d / 32) * 32 * 33;
     L.sig = o;   o = align16(o + sigf * 4);
-    L.wsm = o;   o = align16(o + NW * 32 * 36 * 4);    // per-warp W1 block, rows padded to 36
+    L.wsm = o;   o = align16(o + NW * 32 * 33 * 4);    // per-warp W1 transpose tile (padded)
   } else {
     L.xs = o;    o = align16(o + T * (n + 1) * d * 4); // X, later G rows
     L.pg = L.xs;
@@ -78,6 +78,9 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.spos = o;  o = align16(o + kMaxKeys * 2);
   L.misc = o;  o = align16(o + 16 * 4);
   L.amask = o; o = align16(o + 2 * kMaxKeys * (kMaxKeys / 32) * 4);   // per hash slot: member positions
+  L.pu = o;    o = align16(o + kMaxKeys * 4);     // position -> distinct row index
+  L.urow = o;  o = align16(o + kMaxKeys * 4);     // distinct row index -> row
+  L.uslot = o; o = align16(o + kMaxKeys * 4);     // distinct row index -> hash slot
   L.ws = o;    o = align16(o + 64 * 4);
   L.red = o;   o = align16(o + 2 * 32 * 32 * 4);
   L.total1 = o;
@@ -106,7 +109,6 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.hkey = o;   o = align16(o + HS * 4);
   L.hfirst = o; o = align16(o + HS * 4);
   L.stage = o;  o = align16(o + MCAP * d * 4);
-  L.cstage = o; o = align16(o + 4 * NW * d * 4);     // C rows of each warp's first 4 distinct rows
   L.rmask = o;  o = align16(o + MCAP * (512 / 32) * 4);   // per distinct row: member entries
   const int fast_end = o;
   // sorted fallback (aliases the hash path)
