@@ -1,6 +1,10 @@
 """Build libpg.so (sm_100a) in-tree with plain nvcc -- no torch in the link.
 
-    python -m paper_1404_1521_b200.build [--force]
+    python -m paper_1404_1521_b200.build [--force] [--trace]
+
+`--trace` builds the instrumented variant libpg_trace.so (-DPG_TRACE: per-CTA
+%globaltimer phase stamps, PG_OPT_TRACE), loaded when PG_LIB_VARIANT=trace;
+the production library carries no instrumentation.
 """
 from __future__ import annotations
 
@@ -14,6 +18,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpg.so")
+
+
+def paths(variant: str = ""):
+    if variant == "trace":
+        return os.path.join(HERE, "_build_trace"), os.path.join(HERE, "libpg_trace.so"), ["-DPG_TRACE"]
+    return BUILD, LIB, []
 SOURCES = ["api.cu", "step.cu", "scatter.cu", "nccl_shim.cpp"]
 HEADERS = ["common.cuh", "step.cuh", "scatter.cuh", "nccl_shim.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -41,17 +51,18 @@ def _nvcc():
     return "nvcc"
 
 
-def _stale():
-    if not os.path.exists(LIB):
+def _stale(lib_path=LIB):
+    if not os.path.exists(lib_path):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib_path)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps += [os.path.join(HERE, "..", "include", "pg.h"), __file__]
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+    BUILD, LIB, defs = paths(variant)
+    if not force and not _stale(LIB):
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     inc = ["-I", CSRC, "-I", os.path.join(HERE, "..", "include"), "-I", _nccl_include()]
@@ -61,7 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(BUILD, src + ".o")
         if src.endswith(".cu"):
             cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                   "-Xptxas", "-v", "--expt-relaxed-constexpr", *inc, "-c",
+                   "-Xptxas", "-v", "--expt-relaxed-constexpr", *defs, *inc, "-c",
                    os.path.join(CSRC, src), "-o", obj]
         else:
             cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-I", "/usr/local/cuda/include", *inc, "-c",
@@ -89,4 +100,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                variant="trace" if "--trace" in sys.argv else ""))

@@ -44,13 +44,24 @@ __device__ __forceinline__ size_t list_index(const StepParams& p, int L, int off
 }
 
 // Optional phase timestamps for profiling (PG_OPT_TRACE; thread 0 of each CTA).
+// Phase stamps for scripts/trace_step.py: compiled only into the instrumented
+// library variant (PG_TRACE, libpg_trace.so) -- the production kernel carries
+// no trace code (its instructions would cost instruction-cache space).
+#ifdef PG_TRACE
 __device__ __forceinline__ void trace_mark(const StepParams& p, int k) {
-  if (p.trace != nullptr && threadIdx.x == 0) {
+  if (threadIdx.x == 0 && p.trace != nullptr) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.trace[blockIdx.x * 32 + k] = t;
   }
 }
+__device__ __forceinline__ void trace_clock(const StepParams& p, int k) {
+  if (threadIdx.x == 0 && p.trace != nullptr) p.trace[blockIdx.x * 32 + k] = clock64();
+}
+#else
+__device__ __forceinline__ void trace_mark(const StepParams&, int) {}
+__device__ __forceinline__ void trace_clock(const StepParams&, int) {}
+#endif
 
 // ------------------------------------------------------------------ error reporting
 __device__ __forceinline__ void report_bad(DevStatus* st, long long pos, int value) {
@@ -336,6 +347,7 @@ __device__ __forceinline__ void gather_rows(const StepParams& p, unsigned char* 
     ex = e0 + e;
     row = s < n ? __ldg(p.idx + ex * n + s) : __ldg(p.corr + ex);
   }
+  asm volatile("" ::: "memory");   // keep the index loads ahead of the caller's loads
   wload();   // caller's register loads, queued behind the index loads
   agg_reset(p, sm);
   if (tid < K) {
@@ -394,9 +406,9 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
     return (int)(hi - e0 < T ? (hi - e0 > 0 ? hi - e0 : 0) : T);
   };
   const float b1 = __ldg(p.b1 + lane), w2 = __ldg(p.w2 + lane), b2 = __ldg(p.b2);
-  float dacc[32];
+  float2 dacc[16];   // dW1 rows: dacc[j] = (dW1[wrow0+lane][2j], [2j+1]), FFMA2 pairs
 #pragma unroll
-  for (int u = 0; u < 32; ++u) dacc[u] = 0.f;
+  for (int u = 0; u < 16; ++u) dacc[u] = make_float2(0.f, 0.f);
   float acc_db1 = 0.f, acc_dw2 = 0.f, acc_hinge = 0.f;
 
 #pragma unroll 1
@@ -408,43 +420,45 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
     // This warp's W1 block straight into registers (L2-resident after the first
     // CTA touches it), issued before the gather so its latency is hidden:
     // Wcol[k] = W1[wrow0+k][lane] (forward), Wrow[u] = W1[wrow0+lane][u] (backward).
-    float Wcol[32], Wrow[32];
+    float2 Wcol[16], Wrow[16];   // (k, k+1) pairs for FFMA2
     float* wt = reinterpret_cast<float*>(sm + lay.wsm) + (size_t)warp * 32 * 33;
     gather_rows(
         p, sm, e0, cnt, X, rows_s, r == 0,
         [&]() {   // coalesced: one 128 B W1 row per load
           const float* wg = p.W1 + (size_t)wrow0 * 32;
 #pragma unroll
-          for (int k = 0; k < 32; ++k) Wcol[k] = __ldg(wg + k * 32 + lane);
+          for (int j = 0; j < 16; ++j) Wcol[j] = make_float2(__ldg(wg + (2 * j) * 32 + lane), __ldg(wg + (2 * j + 1) * 32 + lane));
         },
         [&]() {   // Wrow = Wcol transposed across the warp, via a padded smem tile
 #pragma unroll
-          for (int k = 0; k < 32; ++k) wt[k * 33 + lane] = Wcol[k];
+          for (int j = 0; j < 16; ++j) { wt[(2 * j) * 33 + lane] = Wcol[j].x; wt[(2 * j + 1) * 33 + lane] = Wcol[j].y; }
           __syncwarp();
 #pragma unroll
-          for (int u = 0; u < 32; ++u) Wrow[u] = wt[lane * 33 + u];
+          for (int j = 0; j < 16; ++j) Wrow[j] = make_float2(wt[lane * 33 + 2 * j], wt[lane * 33 + 2 * j + 1]);
         });
     if (r == 0) trace_mark(p, 1);
     // ---- forward partials: part[warp][e][u] = sum_k x[e][k] W1[wrow0+k][u]
     float* part = pg;
     for (int e = 0; e < cnt; e += 4) {
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      // even / odd k in the two halves of an FFMA2 pair, folded at the end
+      float2 A0 = make_float2(0.f, 0.f), A1 = A0, A2 = A0, A3 = A0;
       const float4* x0 = reinterpret_cast<const float4*>(xrow(e));
       const float4* x1 = reinterpret_cast<const float4*>(xrow(min(e + 1, cnt - 1)));
       const float4* x2 = reinterpret_cast<const float4*>(xrow(min(e + 2, cnt - 1)));
       const float4* x3 = reinterpret_cast<const float4*>(xrow(min(e + 3, cnt - 1)));
 #pragma unroll
       for (int k4 = 0; k4 < 8; ++k4) {
-        float4 v0 = x0[k4], v1 = x1[k4], v2 = x2[k4], v3 = x3[k4];
-        a0 = fmaf(v0.x, Wcol[4 * k4], a0); a0 = fmaf(v0.y, Wcol[4 * k4 + 1], a0);
-        a0 = fmaf(v0.z, Wcol[4 * k4 + 2], a0); a0 = fmaf(v0.w, Wcol[4 * k4 + 3], a0);
-        a1 = fmaf(v1.x, Wcol[4 * k4], a1); a1 = fmaf(v1.y, Wcol[4 * k4 + 1], a1);
-        a1 = fmaf(v1.z, Wcol[4 * k4 + 2], a1); a1 = fmaf(v1.w, Wcol[4 * k4 + 3], a1);
-        a2 = fmaf(v2.x, Wcol[4 * k4], a2); a2 = fmaf(v2.y, Wcol[4 * k4 + 1], a2);
-        a2 = fmaf(v2.z, Wcol[4 * k4 + 2], a2); a2 = fmaf(v2.w, Wcol[4 * k4 + 3], a2);
-        a3 = fmaf(v3.x, Wcol[4 * k4], a3); a3 = fmaf(v3.y, Wcol[4 * k4 + 1], a3);
-        a3 = fmaf(v3.z, Wcol[4 * k4 + 2], a3); a3 = fmaf(v3.w, Wcol[4 * k4 + 3], a3);
+        const float4 v0 = x0[k4], v1 = x1[k4], v2 = x2[k4], v3 = x3[k4];
+        A0 = __ffma2_rn(make_float2(v0.x, v0.y), Wcol[2 * k4], A0);
+        A1 = __ffma2_rn(make_float2(v1.x, v1.y), Wcol[2 * k4], A1);
+        A2 = __ffma2_rn(make_float2(v2.x, v2.y), Wcol[2 * k4], A2);
+        A3 = __ffma2_rn(make_float2(v3.x, v3.y), Wcol[2 * k4], A3);
+        A0 = __ffma2_rn(make_float2(v0.z, v0.w), Wcol[2 * k4 + 1], A0);
+        A1 = __ffma2_rn(make_float2(v1.z, v1.w), Wcol[2 * k4 + 1], A1);
+        A2 = __ffma2_rn(make_float2(v2.z, v2.w), Wcol[2 * k4 + 1], A2);
+        A3 = __ffma2_rn(make_float2(v3.z, v3.w), Wcol[2 * k4 + 1], A3);
       }
+      const float a0 = A0.x + A0.y, a1 = A1.x + A1.y, a2 = A2.x + A2.y, a3 = A3.x + A3.y;
       part[(warp * T + e) * 32 + lane] = a0;
       if (e + 1 < cnt) part[(warp * T + e + 1) * 32 + lane] = a1;
       if (e + 2 < cnt) part[(warp * T + e + 2) * 32 + lane] = a2;
@@ -458,21 +472,22 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
     for (int e = warp; e < cnt; e += 2 * NW) {
       const int e2 = e + NW;
       const bool two = e2 < cnt;
-      float actx[2] = {0.f, 0.f}, acen[2] = {0.f, 0.f}, acor[2] = {0.f, 0.f};
-      for (int s = 0; s < n; ++s) {
-        if (s == c) continue;
-        for (int b = 0; b < DB; ++b) {
-          actx[0] += part[((s * DB + b) * T + e) * 32 + lane];
-          if (two) actx[1] += part[((s * DB + b) * T + e2) * 32 + lane];
-        }
+      // all (n+1)*DB <= 12 block partials in flight at once, then summed per
+      // category in ascending block order (context | centre | corrupt centre)
+      float v0[12], v1[12];
+#pragma unroll
+      for (int w = 0; w < 12; ++w) {
+        v0[w] = w < NW ? part[(w * T + e) * 32 + lane] : 0.f;
+        v1[w] = (two && w < NW) ? part[(w * T + e2) * 32 + lane] : 0.f;
       }
-      for (int b = 0; b < DB; ++b) {
-        acen[0] += part[((c * DB + b) * T + e) * 32 + lane];
-        acor[0] += part[((n * DB + b) * T + e) * 32 + lane];
-        if (two) {
-          acen[1] += part[((c * DB + b) * T + e2) * 32 + lane];
-          acor[1] += part[((n * DB + b) * T + e2) * 32 + lane];
-        }
+      float actx[2] = {0.f, 0.f}, acen[2] = {0.f, 0.f}, acor[2] = {0.f, 0.f};
+      if (r == 0 && e == 0) trace_mark(p, 27);
+#pragma unroll
+      for (int w = 0; w < 12; ++w) {   // branch-free: +0.0 into the other categories is exact
+        const bool cor = w >= n * DB, cen = !cor && w >= c * DB && w < (c + 1) * DB, ctx = !cor && !cen;
+        acor[0] += cor ? v0[w] : 0.f; acor[1] += cor ? v1[w] : 0.f;
+        acen[0] += cen ? v0[w] : 0.f; acen[1] += cen ? v1[w] : 0.f;
+        actx[0] += ctx ? v0[w] : 0.f; actx[1] += ctx ? v1[w] : 0.f;
       }
       float z[2], zc[2], a[2], ac[2], sp[2], spc[2];
 #pragma unroll
@@ -493,6 +508,7 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
           spc[k] += __shfl_xor_sync(0xffffffffu, spc[k], o);
         }
       }
+      if (r == 0 && e == 0) trace_mark(p, 28);
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         if (k == 1 && !two) break;
@@ -523,23 +539,21 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
       const float xl0 = xrow(e)[lane], xl1 = two ? xrow(e1)[lane] : 0.f;
       const float4* sv0 = reinterpret_cast<const float4*>(sv_base + e * 32);
       const float4* sv1 = reinterpret_cast<const float4*>(sv_base + e1 * 32);
-      float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, h0 = 0.f, h1 = 0.f, h2 = 0.f, h3 = 0.f;
+      float2 G01 = make_float2(0.f, 0.f), G23 = G01, H01 = G01, H23 = G01;
+      const float2 x0p = make_float2(xl0, xl0), x1p = make_float2(xl1, xl1);
 #pragma unroll
       for (int u4 = 0; u4 < 8; ++u4) {
         const float4 v = sv0[u4], w = sv1[u4];
-        g0 = fmaf(Wrow[4 * u4], v.x, g0);
-        g1 = fmaf(Wrow[4 * u4 + 1], v.y, g1);
-        g2 = fmaf(Wrow[4 * u4 + 2], v.z, g2);
-        g3 = fmaf(Wrow[4 * u4 + 3], v.w, g3);
-        h0 = fmaf(Wrow[4 * u4], w.x, h0);
-        h1 = fmaf(Wrow[4 * u4 + 1], w.y, h1);
-        h2 = fmaf(Wrow[4 * u4 + 2], w.z, h2);
-        h3 = fmaf(Wrow[4 * u4 + 3], w.w, h3);
-        dacc[4 * u4] = fmaf(xl1, w.x, fmaf(xl0, v.x, dacc[4 * u4]));
-        dacc[4 * u4 + 1] = fmaf(xl1, w.y, fmaf(xl0, v.y, dacc[4 * u4 + 1]));
-        dacc[4 * u4 + 2] = fmaf(xl1, w.z, fmaf(xl0, v.z, dacc[4 * u4 + 2]));
-        dacc[4 * u4 + 3] = fmaf(xl1, w.w, fmaf(xl0, v.w, dacc[4 * u4 + 3]));
+        const float2 vlo = make_float2(v.x, v.y), vhi = make_float2(v.z, v.w);
+        const float2 wlo = make_float2(w.x, w.y), whi = make_float2(w.z, w.w);
+        G01 = __ffma2_rn(Wrow[2 * u4], vlo, G01);
+        G23 = __ffma2_rn(Wrow[2 * u4 + 1], vhi, G23);
+        H01 = __ffma2_rn(Wrow[2 * u4], wlo, H01);
+        H23 = __ffma2_rn(Wrow[2 * u4 + 1], whi, H23);
+        dacc[2 * u4] = __ffma2_rn(wlo, x1p, __ffma2_rn(vlo, x0p, dacc[2 * u4]));
+        dacc[2 * u4 + 1] = __ffma2_rn(whi, x1p, __ffma2_rn(vhi, x0p, dacc[2 * u4 + 1]));
       }
+      const float g0 = G01.x, g1 = G01.y, g2 = G23.x, g3 = G23.y, h0 = H01.x, h1 = H01.y, h2 = H23.x, h3 = H23.y;
       Gs[(e * (n + 1) + slot) * d + blk * 32 + lane] = (g0 + g1) + (g2 + g3);
       if (two) Gs[(e1 * (n + 1) + slot) * d + blk * 32 + lane] = (h0 + h1) + (h2 + h3);
     }
@@ -554,7 +568,10 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
   float* dsm = sig;   // [DB][32][33]: the corrupt-centre warps' dW1 rows
   if (slot == n) {
 #pragma unroll
-    for (int u = 0; u < 32; ++u) dsm[(blk * 32 + lane) * 33 + u] = dacc[u];
+    for (int u = 0; u < 16; ++u) {
+      dsm[(blk * 32 + lane) * 33 + 2 * u] = dacc[u].x;
+      dsm[(blk * 32 + lane) * 33 + 2 * u + 1] = dacc[u].y;
+    }
   }
   red[warp * 32 + lane] = acc_db1;
   red[32 * 32 + warp * 32 + lane] = acc_dw2;
@@ -563,11 +580,17 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
   if (slot < n) {
     if (slot == c) {
 #pragma unroll
-      for (int u = 0; u < 32; ++u) dacc[u] += dsm[(blk * 32 + lane) * 33 + u];
+      for (int u = 0; u < 16; ++u) {
+        dacc[u].x += dsm[(blk * 32 + lane) * 33 + 2 * u];
+        dacc[u].y += dsm[(blk * 32 + lane) * 33 + 2 * u + 1];
+      }
     }
     float* tile = X + (size_t)warp * 32 * 33;   // X|pg are free: warp-private transpose tile
 #pragma unroll
-    for (int u = 0; u < 32; ++u) tile[lane * 33 + u] = dacc[u];
+    for (int u = 0; u < 16; ++u) {
+      tile[lane * 33 + 2 * u] = dacc[u].x;
+      tile[lane * 33 + 2 * u + 1] = dacc[u].y;
+    }
     __syncwarp();
     float4* dst = reinterpret_cast<float4*>(rec + (size_t)wrow0 * 32);
 #pragma unroll
@@ -1058,18 +1081,17 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
   __syncthreads();
   trace_mark(p, 22);
   const int nrows = rcur[lay.MCAP];
-  // trip 3, issued now: the C values of this thread's first (row, quad) items
+  // trip 3, issued now: the current C rows, staged behind the M partials while
+  // they fit (rows beyond the stage capacity are read directly when applied)
   const int Q = d >> 2;
   const bool quad = (d & 3) == 0;
-  float4 cpre[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int it = tid + k * NT;
-    if (quad && it < nrows * Q) {
-      const int ri = it / Q, q = it - ri * Q;
-      cpre[k] = ldcg4(p.C + (size_t)rrow[ri] * d + 4 * q);
-    }
+  const int ccap = quad ? min(nrows, lay.MCAP - M) : 0;
+  #pragma unroll 2
+  for (int it = tid; it < ccap * Q; it += NT) {
+    const int ri = it / Q, q = it - ri * Q;
+    cp_async16(stage + (size_t)(M + ri) * d + 4 * q, p.C + (size_t)rrow[ri] * d + 4 * q);
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   if (my_r[0] >= 0) rcnt[my_r[0]] = hcnt[my_hs[0]];
   if (my_r[1] >= 0) rcnt[my_r[1]] = hcnt[my_hs[1]];
   #pragma unroll 1
@@ -1106,20 +1128,16 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
   // per (row, feature quad) when d % 4 == 0, else one warp per row
   if (quad) {
     const float4* S4 = reinterpret_cast<const float4*>(stage);
-    auto item = [&](int it, bool pre, float4 o) {
+#pragma unroll 1
+    for (int it = tid; it < nrows * Q; it += NT) {
       const int ri = it / Q, q = it - ri * Q;
       const float4 a = ordered_quadsum(S4, hlist + roff[ri], rcnt[ri], Q, q);
       if (write) {
         float4* c4 = reinterpret_cast<float4*>(p.C + (size_t)rrow[ri] * d) + q;
-        if (!pre) o = __ldcg(c4);
+        const float4 o = ri < ccap ? S4[(size_t)(M + ri) * Q + q] : __ldcg(c4);
         *c4 = make_float4(o.x + nlr * a.x, o.y + nlr * a.y, o.z + nlr * a.z, o.w + nlr * a.w);
       }
-    };
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (tid + k * NT < nrows * Q) item(tid + k * NT, true, cpre[k]);
-#pragma unroll 1
-    for (int it = tid + 4 * NT; it < nrows * Q; it += NT) item(it, false, make_float4(0.f, 0.f, 0.f, 0.f));
+    }
   } else {
 #pragma unroll 1
     for (int ri = warp; ri < nrows; ri += NW) {
@@ -1338,7 +1356,7 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
   }
   __syncthreads();
   trace_mark(p, 0);
-  if (p.trace != nullptr && threadIdx.x == 0) p.trace[blockIdx.x * 32 + 12] = clock64();
+  trace_clock(p, 12);
   if (phases & 1) {
     if (FAST) phase1_fast(p, smem);
     else phase1_generic(p, smem);
@@ -1351,7 +1369,7 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
   if (phases & 2) phase2(p, smem);
   __syncthreads();
   trace_mark(p, 11);
-  if (p.trace != nullptr && threadIdx.x == 0) p.trace[blockIdx.x * 32 + 13] = clock64();
+  trace_clock(p, 13);
 }
 
 int step_fast_ok(int d, int n, int h) {

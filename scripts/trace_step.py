@@ -1,9 +1,10 @@
-"""Per-CTA phase timestamps of the fused step (PG_OPT_TRACE), averaged over steps."""
+"""Per-CTA phase timestamps of the fused step (PG_OPT_TRACE, libpg_trace.so), averaged over steps."""
 import argparse
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["PG_LIB_VARIANT"] = "trace"   # instrumented build: python -m paper_1404_1521_b200.build --trace
 import numpy as np
 import torch
 
@@ -36,20 +37,20 @@ for t in range(a.steps):
 torch.cuda.synchronize()
 names = ["start", "gathered", "fwd", "sigma", "bwd", "agg", "p1end", "barrier", "p2head", "dense", "", "end",
          "", "", "agg.ins", "agg.scan", "agg.place", "agg.acc", "agg.csr", "idx",
-         "m.esrc", "m.trip2", "m.hash", "m.scan", "m.trip3", "g.rows", "w1"]
+         "m.esrc", "m.trip2", "m.hash", "m.scan", "m.trip3", "g.rows", "w1", "s.loaded", "s.shfl"]
 X = tr.view(a.steps, 160, 32).cpu().numpy()[2:, :P].astype(np.float64)
 rel = []
 mhz = []
 for x in X:
     t0 = x[:, 0].min()
-    y = x[:, :27].copy()
+    y = x[:, :29].copy()
     y[:, 12:14] = 0
     rel.append(np.where(y > 0, y - t0, np.nan))
     mhz.append(np.median((x[:, 13] - x[:, 12]) / (x[:, 11] - x[:, 0]) * 1e3))
 A = np.stack(rel)
 print(f"B={a.batch} split={a.split} flush={a.flush} busy={a.busy} SM clock in kernel ~{np.median(mhz):.0f} MHz "
       f"(us from earliest CTA start; median / max over CTAs)")
-order = [0, 19, 25, 26, 1, 2, 3, 4, 14, 15, 16, 18, 17, 5, 6, 7, 8, 9, 20, 21, 22, 23, 24, 11]
+order = [0, 19, 25, 26, 1, 2, 27, 28, 3, 4, 14, 15, 16, 18, 17, 5, 6, 7, 8, 9, 20, 21, 22, 23, 24, 11]
 for k in order:
     nm = names[k]
     col = A[:, :, k]
