@@ -52,18 +52,31 @@ __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void grid_barrier(unsigned long long* arrivals) {
+// Split form: grid_arrive publishes this CTA's prior writes and returns (in
+// thread 0) the instance's release count; independent work can run before
+// grid_wait blocks on it.
+__device__ __forceinline__ unsigned long long grid_arrive(unsigned long long* arrivals) {
   __syncthreads();
+  unsigned long long target = 0;
   if (threadIdx.x == 0) {
     unsigned long long old;
     asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(arrivals) : "memory");
-    const unsigned long long G = gridDim.x, target = (old / G + 1) * G;
-    unsigned long long now = old + 1;
-    while (now < target) {
+    const unsigned long long G = gridDim.x;
+    target = (old / G + 1) * G;
+  }
+  return target;
+}
+__device__ __forceinline__ void grid_wait(unsigned long long* arrivals, unsigned long long target) {
+  if (threadIdx.x == 0) {
+    unsigned long long now;
+    do {
       asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(now) : "l"(arrivals) : "memory");
-    }
+    } while (now < target);
   }
   __syncthreads();
+}
+__device__ __forceinline__ void grid_barrier(unsigned long long* arrivals) {
+  grid_wait(arrivals, grid_arrive(arrivals));
 }
 
 // ---------------------------------------------------------------- mbarrier + bulk copy (TMA engine)

@@ -165,18 +165,20 @@ __device__ __forceinline__ float4 ordered_quadsum(const float4* src, const unsig
   float4 a[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) a[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  // 8 positions per trip (two per chain, in order) so long lists keep 8 loads in flight
 #pragma unroll 1
-  for (int i = 0; i < m; i += 4) {
-    float4 v[4];
+  for (int i = 0; i < m; i += 8) {
+    float4 v[8];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) v[c] = src[(size_t)pos[i + c < m ? i + c : i] * Q + q];
+    for (int c = 0; c < 8; ++c) v[c] = src[(size_t)pos[i + c < m ? i + c : i] * Q + q];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 8; ++c) {
       const bool ok = i + c < m;
-      a[c].x += ok ? v[c].x : 0.f;
-      a[c].y += ok ? v[c].y : 0.f;
-      a[c].z += ok ? v[c].z : 0.f;
-      a[c].w += ok ? v[c].w : 0.f;
+      float4& t = a[c & 3];
+      t.x += ok ? v[c].x : 0.f;
+      t.y += ok ? v[c].y : 0.f;
+      t.z += ok ? v[c].z : 0.f;
+      t.w += ok ? v[c].w : 0.f;
     }
   }
   return make_float4((a[0].x + a[1].x) + (a[2].x + a[3].x), (a[0].y + a[1].y) + (a[2].y + a[3].y),
@@ -990,47 +992,46 @@ __device__ int det_counts(const StepParams& p, unsigned char* sm, int pre_a, int
   return running;
 }
 
-// Deterministic owner merge (hash fast path, M <= MCAP): CTA q owns rows with
-// row % P == q.  Its entries are staged in (list, position) order -- list
-// order is the fixed summation order -- and each distinct row's partials are
-// summed in that order, then C[row] += -lr * sum (one rounding).
-__device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool write) {
+// Phase-2 table resets: CTA-local, so they run between the grid-barrier arrive
+// and wait (phase 1's shared memory is dead by then).  Needs a barrier before use.
+__device__ void phase2_prep(const StepParams& p, unsigned char* sm) {
   const Layout& lay = p.lay;
-  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  int* hkey = reinterpret_cast<int*>(sm + lay.hkey);
+  int* hfirst = reinterpret_cast<int*>(sm + lay.hfirst);
+  #pragma unroll 1
+  for (int i = tid; i < lay.HS; i += NT) { hkey[i] = -1; hfirst[i] = 0; }
+  uint4* rmask = reinterpret_cast<uint4*>(sm + lay.rmask);
+  #pragma unroll 1
+  for (int i = tid; i < lay.MCAP * 4; i += NT) rmask[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (tid == 0) reinterpret_cast<int*>(sm + lay.rcur)[lay.MCAP] = 0;
+}
+
+// Issue half: entry sources, then trip 2 (row ids, then the gradient partials)
+// as cp.async groups -- returns at once so the dense update runs while they are
+// in flight.
+__device__ void det_issue(const StepParams& p, unsigned char* sm, int M) {
+  const Layout& lay = p.lay;
+  const int tid = threadIdx.x, NT = blockDim.x;
   const int d = p.d, NL = p.NLtot;
   const int* lbase = reinterpret_cast<const int*>(sm + lay.lbase);
   const int* loff = reinterpret_cast<const int*>(sm + lay.loff);
-  int* ws = reinterpret_cast<int*>(sm + lay.ws2);
   int* esrc = reinterpret_cast<int*>(sm + lay.esrc);
   int* erow = reinterpret_cast<int*>(sm + lay.erow);
-  int* heads = reinterpret_cast<int*>(sm + lay.heads);
-  unsigned short* hlist = reinterpret_cast<unsigned short*>(sm + lay.hlist);
   int* hkey = reinterpret_cast<int*>(sm + lay.hkey);
   int* hfirst = reinterpret_cast<int*>(sm + lay.hfirst);
   float* stage = reinterpret_cast<float*>(sm + lay.stage);
-  const int HS = lay.HS;
-  const float nlr = -p.lr;
   #pragma unroll 1
-  for (int e = tid; e < M; e += NT) {
-    int lo = 0, hi = NL - 1;   // last L with lbase[L] <= e
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (lbase[mid] <= e) lo = mid; else hi = mid - 1;
-    }
-    esrc[e] = (int)list_index(p, lo, loff[lo] + (e - lbase[lo]));
+  for (int L = tid; L < NL; L += NT) {   // entries of list L: [lbase[L], lbase[L+1])
+    const int b = lbase[L], cnt = lbase[L + 1] - b;
+    #pragma unroll 1
+    for (int j = 0; j < cnt; ++j) esrc[b + j] = (int)list_index(p, L, loff[L] + j);
   }
+  __syncthreads();
   trace_mark(p, 20);
   #pragma unroll 1
-  for (int i = tid; i < HS; i += NT) { hkey[i] = -1; hfirst[i] = 0; }
-  unsigned* rmask = reinterpret_cast<unsigned*>(sm + lay.rmask);
-  #pragma unroll 1
-  for (int i = tid; i < lay.MCAP * 4; i += NT) reinterpret_cast<uint4*>(rmask)[i] = make_uint4(0u, 0u, 0u, 0u);
-  if (tid == 0) reinterpret_cast<int*>(sm + lay.rcur)[lay.MCAP] = 0;
-  __syncthreads();
-  // ---- trip 2: row ids and gradient partials of all entries at once (cp.async:
-  // lower latency than per-row bulk copies for these L2-resident records)
-  #pragma unroll 1
-  for (int e = tid; e < M; e += NT) erow[e] = __ldcg(p.list_rows + esrc[e]);
+  for (int e = tid; e < M; e += NT) cp_async4(erow + e, p.list_rows + esrc[e]);
+  asm volatile("cp.async.commit_group;" ::: "memory");
   if ((d & 3) == 0) {
     const int Q = d >> 2;
     #pragma unroll 2
@@ -1046,6 +1047,29 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Deterministic owner merge (hash fast path, M <= MCAP): CTA q owns rows with
+// row % P == q.  Its entries are staged in (list, position) order -- list
+// order is the fixed summation order -- and each distinct row's partials are
+// summed in that order, then C[row] += -lr * sum (one rounding).  Runs after
+// det_issue.
+__device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool write) {
+  const Layout& lay = p.lay;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  const int d = p.d;
+  int* ws = reinterpret_cast<int*>(sm + lay.ws2);
+  int* esrc = reinterpret_cast<int*>(sm + lay.esrc);
+  int* erow = reinterpret_cast<int*>(sm + lay.erow);
+  int* heads = reinterpret_cast<int*>(sm + lay.heads);
+  unsigned short* hlist = reinterpret_cast<unsigned short*>(sm + lay.hlist);
+  int* hkey = reinterpret_cast<int*>(sm + lay.hkey);
+  int* hfirst = reinterpret_cast<int*>(sm + lay.hfirst);
+  float* stage = reinterpret_cast<float*>(sm + lay.stage);
+  const int HS = lay.HS;
+  const float nlr = -p.lr;
+  unsigned* rmask = reinterpret_cast<unsigned*>(sm + lay.rmask);
+  asm volatile("cp.async.wait_group 1;" ::: "memory");   // row ids landed (partials may still fly)
   __syncthreads();
   trace_mark(p, 21);
   // ---- distinct rows: smem hash (row -> distinct index), multiplicity per row
@@ -1196,38 +1220,27 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
   __shared__ float s_loss;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x;
   DevStatus* st = p.st;
-  // ---- trip 1: everything that does not depend on the decision
+  // ---- trip 1: everything that does not depend on the decision, all issued
+  // before any of it is consumed (one round trip, not one per consumer)
   unsigned my_done = 0;
+  int f0 = 0;
+  unsigned long long bad = 0;
   if (tid == 0) {
-    int f = __ldcg(&st->flags);
-    const unsigned long long bad = __ldcg(&st->bad);
-    if (p.flags_from_records) {   // data parallel: every rank skips together
-      f = 0;
-      for (int r = 0; r < p.Ptot; ++r)
-        f |= __float_as_int(__ldcg(p.dense_part + (size_t)r * p.dense_stride + p.dense_len + 1));
-    }
-    s_flags = f;
-    if (blockIdx.x == 0) st->last_bad = bad;
+    f0 = __ldcg(&st->flags);
+    bad = __ldcg(&st->bad);
     my_done = atomicAdd(&st->done, 1u);   // result consumed only at the end (flag reset)
   }
+  const int hoff = p.dense_len;   // record words [hoff, hoff+1] = (hinge sum, flags); hoff is even
+  float2 hv[5];   // warp 1: the first 160 records' (hinge, flags)
   if (warp == 1) {
-    float acc = 0.f;
-    const int hoff = p.dense_len;
-    #pragma unroll 1
-    for (int r0 = 0; r0 < p.Ptot; r0 += 32 * 5) {   // 5 loads in flight per lane
-      float v[5];
 #pragma unroll
-      for (int k = 0; k < 5; ++k) {
-        const int r = r0 + lane + 32 * k;
-        v[k] = r < p.Ptot ? __ldcg(p.dense_part + (size_t)r * p.dense_stride + hoff) : 0.f;
-      }
-#pragma unroll
-      for (int k = 0; k < 5; ++k) acc += v[k];
+    for (int k = 0; k < 5; ++k) {
+      const int r = lane + 32 * k;
+      hv[k] = r < p.Ptot ? __ldcg(reinterpret_cast<const float2*>(p.dense_part + (size_t)r * p.dense_stride + hoff))
+                         : make_float2(0.f, 0.f);
     }
-    acc = warp_sum(acc);
-    if (lane == 0) s_loss = acc * p.inv_B;
   }
-  // owner counts for lists [0, NT): issued before anything consumes a load
+  // owner counts for lists [0, NT)
   int pre_a = 0, pre_b = 0;
   if (p.mode == 0 && tid < p.NLtot) {
     const int32_t* off = p.list_off + (size_t)tid * (p.P + 1) + blockIdx.x;
@@ -1240,16 +1253,42 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
   float4 dacc0 = make_float4(0.f, 0.f, 0.f, 0.f);
   float cur0[4] = {0.f, 0.f, 0.f, 0.f};
   if (nq0 > 0) {
-    dacc0 = dense_partial(p, ds.q0, nq0, groups0);
-    if (tid < nq0) {
+    if (tid < nq0) {   // the parameters this CTA updates
       const int ndh = p.n * p.d * p.h, base = 4 * (ds.q0 + tid);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         if (base + k < p.dense_len) cur0[k] = __ldcg(param_ptr(p, base + k, ndh));
     }
+    dacc0 = dense_partial(p, ds.q0, nq0, groups0);   // issues its loads, then sums
   }
+  if (warp == 1) {   // mean hinge, summed in record order; OR of the records' flags
+    float acc = 0.f;
+    unsigned fl = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) { acc += hv[k].x; fl |= (unsigned)__float_as_int(hv[k].y); }
+    #pragma unroll 1
+    for (int r0 = 160; r0 < p.Ptot; r0 += 32) {   // only with many ranks
+      const int r = r0 + lane;
+      const float2 v = r < p.Ptot ? __ldcg(reinterpret_cast<const float2*>(p.dense_part + (size_t)r * p.dense_stride + hoff))
+                                  : make_float2(0.f, 0.f);
+      acc += v.x;
+      fl |= (unsigned)__float_as_int(v.y);
+    }
+    acc = warp_sum(acc);
+    fl = __reduce_or_sync(0xffffffffu, fl);
+    if (lane == 0) {
+      s_loss = acc * p.inv_B;
+      if (p.flags_from_records) s_flags = (int)fl;   // data parallel: every rank skips together
+    }
+  }
+  if (tid == 0) {
+    if (!p.flags_from_records) s_flags = f0;
+    if (blockIdx.x == 0) st->last_bad = bad;
+  }
+  trace_mark(p, 29);
   int M = 0;
   if (p.mode == 0) M = det_counts(p, sm, pre_a, pre_b);   // contains __syncthreads
+  trace_mark(p, 30);
   __syncthreads();
   const float loss = s_loss;
   const int flags = s_flags | (!isfinite(loss) ? 2 : 0);
@@ -1265,6 +1304,8 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
     }
   }
   trace_mark(p, 8);
+  const bool hashed = p.mode == 0 && M > 0 && M <= p.lay.MCAP;
+  if (hashed) det_issue(p, sm, M);   // trip 2 in flight during the dense update
   // ---- dense update (first block prefetched; further blocks only when P is small)
   if (nq0 > 0) dense_apply(p, sm, ds.q0, nq0, groups0, dacc0, make_float4(cur0[0], cur0[1], cur0[2], cur0[3]), write);
   #pragma unroll 1
@@ -1283,10 +1324,8 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
   trace_mark(p, 9);
   // ---- embedding scatter-add
   if (p.mode == 0) {
-    if (M > 0) {
-      if (M <= p.lay.MCAP) det_merge(p, sm, M, write);
-      else if (write) scatter_det_sorted(p, sm);
-    }
+    if (hashed) det_merge(p, sm, M, write);
+    else if (M > 0 && write) scatter_det_sorted(p, sm);
   } else if (write) {
     phase2_scatter_atomic(p);
   }
@@ -1363,7 +1402,15 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
     __syncthreads();
     trace_mark(p, 6);
   }
-  if ((phases & 1) && (phases & 6)) grid_barrier(&p.st->bar_arrivals);
+  const bool prep = (phases & 2) && p.mode == 0;
+  if ((phases & 1) && (phases & 6)) {
+    const unsigned long long target = grid_arrive(&p.st->bar_arrivals);
+    if (prep) phase2_prep(p, smem);   // overlaps the barrier
+    grid_wait(&p.st->bar_arrivals, target);
+  } else if (prep) {
+    phase2_prep(p, smem);
+    __syncthreads();
+  }
   trace_mark(p, 7);
   if (phases & 4) build_record(p, smem);
   if (phases & 2) phase2(p, smem);

@@ -9,22 +9,34 @@ constexpr int kTMax = 32;       // examples per chunk
 constexpr int kMaxKeys = 256;   // (n+1)*T <= 256 gradient rows per chunk
 constexpr int kCapK = 2048;     // phase-2 owner-merge keys per window (sorted fallback)
 
-// Device-resident status / synchronisation block (one per model).
+// Device-resident status / synchronisation block (one per model).  Words that
+// all CTAs hit in the same phase live in separate 128 B lines: the barrier
+// counter is polled by every CTA, `done` takes one atomic per CTA, and the
+// current-step error words are read once per CTA -- sharing a line made those
+// accesses serialise at one L2 slice.
 struct DevStatus {
-  unsigned long long bad;        // current step: min over (pos << 32 | uint32 value)
-  unsigned long long last_bad;   // result of the most recent step
+  // line 0: current step's error state (phase 1 writes on error; phase 2 reads)
+  unsigned long long bad;        // min over (pos << 32 | uint32 value)
+  int flags;                     // bit0 bad index
+  int pad0[29];
+  // line 1: grid barrier -- monotonic arrival count (never reset)
+  alignas(128) unsigned long long bar_arrivals;
+  unsigned long long pad1[15];
+  // line 2: phase-2 arrival counter (flag-reset protocol)
+  alignas(128) unsigned done;
+  unsigned pad2[31];
+  // line 3: results of the most recent step, sticky state, pg_score check
+  alignas(128) unsigned long long last_bad;
   unsigned long long sticky_bad; // min over asynchronous steps since pg_sync
   unsigned long long score_bad;  // pg_score index check
-  unsigned long long bar_arrivals; // grid barrier: monotonic arrival count (never reset)
-  unsigned done;                 // phase-2 arrival counter (flag-reset protocol)
-  int flags;                     // current step: bit0 bad index
   int last_flags;                // most recent step: bit0 bad index, bit1 non-finite loss
   int sticky_flags;              // OR over asynchronous steps since pg_sync
   int rank_flags;                // data-parallel: OR over all ranks
   int score_flags;
   float last_loss;
-  int pad[3];
+  int pad3[21];
 };
+static_assert(sizeof(DevStatus) == 512, "DevStatus: four 128 B lines");
 
 // Shared-memory carve-up (byte offsets), computed once on the host.
 struct Layout {

@@ -37,20 +37,20 @@ for t in range(a.steps):
 torch.cuda.synchronize()
 names = ["start", "gathered", "fwd", "sigma", "bwd", "agg", "p1end", "barrier", "p2head", "dense", "", "end",
          "", "", "agg.ins", "agg.scan", "agg.place", "agg.acc", "agg.csr", "idx",
-         "m.esrc", "m.trip2", "m.hash", "m.scan", "m.trip3", "g.rows", "w1", "s.loaded", "s.shfl"]
+         "m.esrc", "m.trip2", "m.hash", "m.scan", "m.trip3", "g.rows", "w1", "s.loaded", "s.shfl", "p2.dense_ld", "p2.counts"]
 X = tr.view(a.steps, 160, 32).cpu().numpy()[2:, :P].astype(np.float64)
 rel = []
 mhz = []
 for x in X:
     t0 = x[:, 0].min()
-    y = x[:, :29].copy()
+    y = x[:, :31].copy()
     y[:, 12:14] = 0
     rel.append(np.where(y > 0, y - t0, np.nan))
     mhz.append(np.median((x[:, 13] - x[:, 12]) / (x[:, 11] - x[:, 0]) * 1e3))
 A = np.stack(rel)
 print(f"B={a.batch} split={a.split} flush={a.flush} busy={a.busy} SM clock in kernel ~{np.median(mhz):.0f} MHz "
       f"(us from earliest CTA start; median / max over CTAs)")
-order = [0, 19, 25, 26, 1, 2, 27, 28, 3, 4, 14, 15, 16, 18, 17, 5, 6, 7, 8, 9, 20, 21, 22, 23, 24, 11]
+order = [0, 19, 25, 26, 1, 2, 27, 28, 3, 4, 14, 15, 16, 18, 17, 5, 6, 7, 29, 30, 8, 9, 20, 21, 22, 23, 24, 11]
 for k in order:
     nm = names[k]
     col = A[:, :, k]
