@@ -57,3 +57,15 @@ for k in order:
     if np.isnan(col).all():
         continue
     print(f"  {nm:9s} med {np.nanmedian(col) / 1e3:7.2f}  max {np.nanmean(np.nanmax(col, axis=1)) / 1e3:7.2f}")
+
+# slowest CTAs (last step): end time, owner entry count M, per-stage deltas
+x = X[-1]
+t0 = x[:, 0].min()
+ends = (x[:, 11] - t0) / 1e3
+slow = np.argsort(-ends)[:6]
+print("slowest CTAs (last step): cta end_us M | trip2 hash scan trip3 sums (us)")
+for b in slow:
+    st = [(x[b, k2] - x[b, k1]) / 1e3 for k1, k2 in ((20, 21), (21, 22), (22, 23), (23, 24), (24, 11))]
+    print(f"  {b:4d} {ends[b]:6.2f} {int(x[b, 31]):4d} | " + " ".join(f"{v:5.2f}" for v in st))
+med = np.median(X[-1][:, 31])
+print(f"median M {med:.0f}, max M {X[-1][:, 31].max():.0f}")
