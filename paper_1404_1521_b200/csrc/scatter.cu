@@ -467,94 +467,105 @@ __global__ void sc_validate(const int32_t* __restrict__ I, int64_t n, int64_t ro
   }
 }
 
-// Tile-local pre-aggregation (ATOMIC mode, cols % 4 == 0, cols <= 128): a CTA
-// takes 256 consecutive entries, finds their distinct rows with an smem hash,
-// sums the Y rows per distinct row with shared-memory atomics (Y read once,
-// coalesced), then issues one red.global.add.v4.f32 per 16 B of each distinct
-// row.  A Zipf head row appears ~20x per tile, so its global reductions drop
-// from one per occurrence to one per tile.
-constexpr int kAggTile = 256;
-__global__ void __launch_bounds__(256) sc_atomic_agg(const int32_t* __restrict__ I, const float* __restrict__ Y,
-                                                     float* W, int cols, int64_t n, const ScatterStatus* st) {
-  extern __shared__ __align__(16) float acc_sm[];   // [kAggTile / 2][cols] duplicated-row sums
-  __shared__ int hk[2 * kAggTile], hs[2 * kAggTile], slot_of[kAggTile], slot_row[kAggTile], slot_cnt[kAggTile];
-  __shared__ int slot_m[kAggTile], mrow[kAggTile / 2];
-  __shared__ int nslots, nmulti;
-  if (*(volatile const int*)&st->flag) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// Cooperative ATOMIC scatter (cols % 4 == 0, cols <= 128): one launch.
+// Every CTA first checks its grid-strided share of I; after a grid barrier all
+// CTAs see the same error flag, so a bad index still means "nothing applied".
+// Then each CTA takes kAtTile consecutive entries per round, finds the rows that
+// occur more than once in its tile (smem hash with counts), sums those rows'
+// Y entries in shared memory and flushes each with one red.global.add.v4.f32
+// per 16 B; rows seen once go straight from Y (streamed, read once) to W with
+// vector reductions.  Zipf head rows thus cost one global reduction per tile,
+// and uniform traffic stays a single streaming pass.
+template <int kAtThreads, int kAtTile, int kAtHash>
+__global__ void __launch_bounds__(kAtThreads) sc_atomic_coop(const int32_t* __restrict__ I,
+                                                             const float* __restrict__ Y, float* W,
+                                                             int64_t rows, int cols, int64_t n, int amax,
+                                                             ScatterStatus* st) {
+  constexpr int kAtAcc = 160;
+  extern __shared__ __align__(16) unsigned char at_sm[];
+  int* hk = reinterpret_cast<int*>(at_sm);                 // [kAtHash]
+  int* hc = hk + kAtHash;                                  // [kAtHash] count, then accumulator (-1: direct)
+  int* sI = hc + kAtHash;                                  // [kAtTile]
+  short* eslot = reinterpret_cast<short*>(sI + kAtTile);   // [kAtTile]
+  float* acc = reinterpret_cast<float*>(eslot + kAtTile);  // [kAtAcc][cols]
+  __shared__ int arow[kAtAcc];
+  __shared__ int nacc;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NWp = kAtThreads / 32;
   const int q = cols >> 2;
-  const int G = q >= 32 ? 32 : q, per = 32 / G, sub = lane / G, gl = lane % G;   // lanes per entry
-  const int64_t ntiles = (n + kAggTile - 1) / kAggTile;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t base = tile * kAggTile;
-    const int cnt = (int)(n - base < kAggTile ? n - base : kAggTile);
-    for (int i = tid; i < 2 * kAggTile; i += 256) hk[i] = -1;
-    if (tid == 0) { nslots = 0; nmulti = 0; }
+  const int G = q >= 32 ? 32 : q, per = 32 / G, sub = lane / G, gl = lane % G;
+  for (int64_t e = (int64_t)blockIdx.x * kAtThreads + tid; e < n; e += (int64_t)gridDim.x * kAtThreads) {
+    const int key = __ldg(I + e);
+    if (key < 0 || (int64_t)key >= rows) {
+      atomicMin(&st->bad, ((unsigned long long)e << 32) | (unsigned)key);
+      atomicOr(&st->flag, 1);
+    }
+  }
+  grid_barrier(&st->arrivals);
+  if (*(volatile const int*)&st->flag) return;
+  const float4* Y4 = reinterpret_cast<const float4*>(Y);
+  for (int64_t base = (int64_t)blockIdx.x * kAtTile; base < n; base += (int64_t)gridDim.x * kAtTile) {
+    const int cnt = (int)(n - base < kAtTile ? n - base : kAtTile);
+    for (int i = tid; i < kAtHash; i += kAtThreads) { hk[i] = -1; hc[i] = 0; }
+    if (tid == 0) nacc = 0;
     __syncthreads();
-    if (tid < cnt) {
-      const int row = __ldg(I + base + tid);
-      unsigned h = ((unsigned)row * 2654435761u) & (2 * kAggTile - 1);
+    for (int i = tid; i < cnt; i += kAtThreads) {
+      const int row = __ldg(I + base + i);
+      sI[i] = row;
+      unsigned h = ((unsigned)row * 2654435761u) & (kAtHash - 1);
       while (true) {
         const int prev = atomicCAS(&hk[h], -1, row);
-        if (prev == -1) {
-          const int sidx = atomicAdd(&nslots, 1);
-          hs[h] = sidx;
-          slot_row[sidx] = row;
-          slot_cnt[sidx] = 0;
-          break;
+        if (prev == -1 || prev == row) break;
+        h = (h + 1) & (kAtHash - 1);
+      }
+      atomicAdd(&hc[h], 1);
+      eslot[i] = (short)h;
+    }
+    __syncthreads();
+    // accumulators go to the most repeated rows first (count >= 16, >= 4, >= 2);
+    // hc[s] becomes -(accumulator index) - 2 for a chosen row, a count otherwise
+    for (int lo : {16, 4, 2}) {
+      for (int s = tid; s < kAtHash; s += kAtThreads) {
+        const int c = hc[s];
+        if (hk[s] != -1 && c >= lo) {
+          const int a = atomicAdd(&nacc, 1);
+          if (a < amax) { arow[a] = hk[s]; hc[s] = -a - 2; }
         }
-        if (prev == row) break;
-        h = (h + 1) & (2 * kAggTile - 1);
       }
-      slot_of[tid] = (int)h;
+      __syncthreads();
     }
+    for (int s = tid; s < kAtHash; s += kAtThreads) hc[s] = hc[s] <= -2 ? -hc[s] - 2 : -1;
     __syncthreads();
-    const int ns = nslots;
-    if (tid < cnt) {
-      const int sl = hs[slot_of[tid]];
-      slot_of[tid] = sl;
-      atomicAdd(&slot_cnt[sl], 1);
-    }
+    const int na = nacc < amax ? nacc : amax;
+    for (int t = tid; t < na * q; t += kAtThreads) reinterpret_cast<float4*>(acc)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
-    // duplicated rows get a compact accumulator (a tile has at most 128 of them)
-    if (tid < ns) {
-      if (slot_cnt[tid] > 1) {
-        const int mid = atomicAdd(&nmulti, 1);
-        slot_m[tid] = mid;
-        mrow[mid] = slot_row[tid];
-      } else {
-        slot_m[tid] = -1;
+    // stream the tile's Y rows once: lane group `sub` takes entries e, e + per, ...
+    // (4 in flight per lane), one float4 per lane (q <= 32 quads per row)
+    constexpr int U = 4;
+    for (int e0 = warp * per * U; e0 < cnt; e0 += NWp * per * U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * per + sub;
+        v[u] = (sub < per && e < cnt && gl < q) ? __ldcs(Y4 + (size_t)(base + e) * q + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-    }
-    __syncthreads();
-    const int nm = nmulti;
-    for (int t = tid; t < nm * q; t += 256) reinterpret_cast<float4*>(acc_sm)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncthreads();
-    // rows seen once: straight vector reductions from Y; duplicated rows: smem sums
-    const float4* y4 = reinterpret_cast<const float4*>(Y + (size_t)base * cols);
-    for (int e0 = warp * per; e0 < cnt; e0 += 8 * per) {
-      const int e = e0 + sub;
-      if (sub < per && e < cnt) {
-        const int sl = slot_of[e];
-        const int mid = slot_m[sl];
-        if (mid < 0) {
-          float* dst = W + (size_t)slot_row[sl] * cols;
-          for (int f = gl; f < q; f += G) red_add_v4(dst + 4 * f, __ldg(y4 + (size_t)e * q + f));
-        } else {
-          float* a = acc_sm + (size_t)mid * cols;
-          for (int f = gl; f < q; f += G) {
-            const float4 v = __ldg(y4 + (size_t)e * q + f);
-            atomicAdd(a + 4 * f, v.x); atomicAdd(a + 4 * f + 1, v.y);
-            atomicAdd(a + 4 * f + 2, v.z); atomicAdd(a + 4 * f + 3, v.w);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * per + sub;
+        if (sub < per && e < cnt && gl < q) {
+          const int a = hc[eslot[e]];
+          if (a < 0) {
+            red_add_v4(W + (size_t)sI[e] * cols + 4 * gl, v[u]);
+          } else {
+            float* d = acc + (size_t)a * cols + 4 * gl;
+            atomicAdd(d, v[u].x); atomicAdd(d + 1, v[u].y); atomicAdd(d + 2, v[u].z); atomicAdd(d + 3, v[u].w);
           }
         }
       }
     }
     __syncthreads();
-    for (int mi = warp; mi < nm; mi += 8) {
-      float* dst = W + (size_t)mrow[mi] * cols;
-      for (int f = lane; f < q; f += 32)
-        red_add_v4(dst + 4 * f, reinterpret_cast<const float4*>(acc_sm + (size_t)mi * cols)[f]);
+    for (int t = tid; t < na * q; t += kAtThreads) {
+      const int a = t / q, f = t - a * q;
+      red_add_v4(W + (size_t)arow[a] * cols + 4 * f, reinterpret_cast<const float4*>(acc)[t]);
     }
     __syncthreads();
   }
@@ -595,6 +606,25 @@ __global__ void sc_atomic_scalar(const int32_t* __restrict__ I, const float* __r
 }
 
 // ------------------------------------------------------------------ host side
+// sc_atomic_coop configuration: (threads, tile entries, hash slots, smem budget).
+// Measured on the 1M-row microbench (Zipf / uniform): 512 x 2048 at 2 CTAs/SM
+// 120 / 93 us; 256 x 1024 at 4/SM 115 / 99 us; 1024 x 8192 at 1/SM 124 / 101 us.
+struct AtCfg {
+  int threads, tile, hash;
+  size_t budget;
+  const void* fn;
+};
+static const AtCfg kAtCfgs[] = {
+    {512, 2048, 4096, 110 * 1024, (const void*)sc_atomic_coop<512, 2048, 4096>},
+};
+static const int g_at_cfg = 0;
+static int g_at_blocks_per_sm = 0;   // sc_atomic_coop occupancy (scatter_prepare)
+static size_t at_fixed(const AtCfg& c) { return sizeof(int) * (2 * c.hash + c.tile) + sizeof(short) * c.tile; }
+static int at_amax(const AtCfg& c, int cols) {   // accumulator rows that fit
+  const int a = (int)((c.budget - at_fixed(c)) / (sizeof(float) * cols));
+  return a < 160 ? a : 160;
+}
+static size_t at_smem(const AtCfg& c, int cols) { return at_fixed(c) + sizeof(float) * at_amax(c, cols) * cols; }
 static int bits_for(int64_t rows) {
   int b = 1;
   while (b < 31 && ((int64_t)1 << b) < rows) ++b;
@@ -657,10 +687,20 @@ cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t ro
   if (e != cudaSuccess) return e;
   const int blocks = pl.num_sms * 4;
   if (mode == 1) {
+    if ((cols & 3) == 0 && cols <= 128 && g_at_blocks_per_sm > 0) {
+      const AtCfg& c = kAtCfgs[g_at_cfg];
+      const size_t smem = at_smem(c, cols);
+      int bps = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, c.fn, c.threads, smem) != cudaSuccess || bps < 1)
+        bps = g_at_blocks_per_sm;
+      int grid = bps * pl.num_sms;
+      int amax = at_amax(c, cols);
+      void* args[] = {(void*)&I, (void*)&Y, (void*)&W, (void*)&rows, (void*)&cols, (void*)&n, (void*)&amax, (void*)&st};
+      *launches += 1;
+      return cudaLaunchCooperativeKernel(c.fn, grid, c.threads, args, smem, s);
+    }
     sc_validate<<<blocks, 256, 0, s>>>(I, n, rows, st);
-    if ((cols & 3) == 0 && cols <= 128)
-      sc_atomic_agg<<<blocks * 2, 256, sizeof(float) * (kAggTile / 2) * cols, s>>>(I, Y, W, cols, n, st);
-    else if ((cols & 3) == 0) sc_atomic<<<blocks * 2, 256, 0, s>>>(I, Y, W, cols, n, st);
+    if ((cols & 3) == 0) sc_atomic<<<blocks * 2, 256, 0, s>>>(I, Y, W, cols, n, st);
     else sc_atomic_scalar<<<blocks * 2, 256, 0, s>>>(I, Y, W, cols, n, st);
     *launches += 2;
     return cudaGetLastError();
@@ -719,9 +759,11 @@ cudaError_t scatter_prepare(int bins) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sc_upsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(int) * (kSortThreads / 32) * bins));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(sc_atomic_agg, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(float) * kAggTile * 128));
+  for (const AtCfg& c : kAtCfgs)
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.budget);
+  if (e == cudaSuccess)   // co-resident CTAs per SM at the largest row width (cols = 128)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_at_blocks_per_sm, kAtCfgs[g_at_cfg].fn,
+                                                      kAtCfgs[g_at_cfg].threads, at_smem(kAtCfgs[g_at_cfg], 128));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sc_reduce<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reduce_smem(4));
   if (e == cudaSuccess)

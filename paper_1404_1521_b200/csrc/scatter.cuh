@@ -10,6 +10,7 @@ struct ScatterStatus {
   int flag;                 // 1: an index was out of range -> nothing applied
   int pad;
   unsigned long long bad;   // min over (position << 32 | uint32 value)
+  unsigned long long arrivals;   // grid-barrier counter of the cooperative atomic kernel
 };
 
 struct ScatterPlan {

@@ -1289,6 +1289,9 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
   int M = 0;
   if (p.mode == 0) M = det_counts(p, sm, pre_a, pre_b);   // contains __syncthreads
   trace_mark(p, 30);
+#ifdef PG_TRACE
+  if (tid == 0 && p.trace != nullptr) p.trace[blockIdx.x * 32 + 31] = M;
+#endif
   __syncthreads();
   const float loss = s_loss;
   const int flags = s_flags | (!isfinite(loss) ? 2 : 0);
