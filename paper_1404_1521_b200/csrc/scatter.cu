@@ -224,6 +224,163 @@ __global__ void __launch_bounds__(kSortThreads) sc_downsweep(
   }
 }
 
+#ifdef PG_TRACE
+__device__ unsigned long long g_sort_tr[160][16];
+#define SORT_MARK(k)                                                                          \
+  do {                                                                                        \
+    if (threadIdx.x == 0) {                                                                   \
+      unsigned long long t_;                                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
+      g_sort_tr[blockIdx.x][k] = t_;                                                          \
+    }                                                                                         \
+  } while (0)
+#else
+#define SORT_MARK(k) do {} while (0)
+#endif
+
+// All radix passes in ONE cooperative launch when the keys fit one tile per CTA
+// (n <= gridDim.x * kSortTile).  Per pass: stable in-tile ranking (warp
+// ballots, as sc_downsweep) with the keys held in registers, tile digit totals
+// to global -> grid barrier -> CTA q scans the tile column of its digit slice
+// (exclusive over tiles) and publishes the digit totals -> grid barrier ->
+// every CTA forms its digit bases and scatters its staged tile with coalesced
+// runs -> grid barrier before the next pass reads the output.  Pass 0 also
+// checks the indices; a bad one stops every CTA after the first barrier.
+// dynamic smem: as sc_downsweep.
+__global__ void __launch_bounds__(kSortThreads) sc_sort_coop(
+    const int32_t* __restrict__ I, int32_t* ka, int32_t* va, int32_t* kb, int32_t* vb, int64_t n,
+    int passes, int bits, int64_t rows, int* cnt, int* tot, ScatterStatus* st) {
+  extern __shared__ int sh[];
+  __shared__ int ws[32];
+  const int bins = 1 << bits;
+  constexpr int NW = kSortThreads / 32;
+  int* whist = sh;
+  int* tpref = whist + NW * bins;
+  int* tstart = tpref + bins;
+  int* skey = tstart + bins;
+  int* sval = skey + kSortTile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x, ntiles = gridDim.x;
+  const int64_t base = (int64_t)tile * kSortTile + (int64_t)warp * 32 * kSortItems;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t rem = n - (int64_t)tile * kSortTile;
+  const int tcnt = (int)(rem < 0 ? 0 : (rem < kSortTile ? rem : kSortTile));
+  SORT_MARK(0);
+  for (int p = 0; p < passes; ++p) {
+    const int shift = p * bits;
+    const int32_t* kin = p == 0 ? I : ((p & 1) ? ka : kb);
+    const int32_t* vin = p == 0 ? nullptr : ((p & 1) ? va : vb);
+    int32_t* kout = (p & 1) ? kb : ka;
+    int32_t* vout = (p & 1) ? vb : va;
+    for (int i = tid; i < NW * bins; i += kSortThreads) whist[i] = 0;
+    __syncthreads();
+    int keys[kSortItems], vals[kSortItems], lrank[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      const int64_t e = base + j * 32 + lane;
+      const bool valid = e < n;
+      keys[j] = valid ? __ldcg(kin + e) : 0;
+      vals[j] = valid ? (vin ? __ldcg(vin + e) : (int)e) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      const int64_t e = base + j * 32 + lane;
+      const bool valid = e < n;
+      if (p == 0 && valid && (keys[j] < 0 || (int64_t)keys[j] >= rows)) {
+        atomicMin(&st->bad, ((unsigned long long)e << 32) | (unsigned)keys[j]);
+        atomicOr(&st->flag, 1);
+        keys[j] = 0;
+      }
+      const unsigned dig = valid ? ((unsigned)keys[j] >> shift) & (bins - 1) : 0u;
+      const unsigned peers = warp_match(dig, bits, valid);
+      const int before = valid ? whist[warp * bins + dig] : 0;
+      __syncwarp();
+      if (valid && (peers & lt) == 0) whist[warp * bins + dig] = before + __popc(peers);
+      __syncwarp();
+      lrank[j] = before + __popc(peers & lt);
+    }
+    __syncthreads();
+    SORT_MARK(1 + 6 * p);
+    // per digit: exclusive over warps (warp order == position order), tile total
+    int tot_d = 0;
+    if (tid < bins) {
+      int h[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) h[w] = whist[w * bins + tid];
+      int run = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        whist[w * bins + tid] = run;
+        run += h[w];
+      }
+      tot_d = run;
+      cnt[(size_t)tid * ntiles + tile] = run;
+    }
+    {
+      int all;
+      const int ex = block_excl_scan(tot_d, ws, &all);
+      if (tid < bins) tstart[tid] = ex;
+    }
+    SORT_MARK(2 + 6 * p);
+    grid_barrier(&st->arrivals);
+    SORT_MARK(3 + 6 * p);
+    if (p == 0 && *(volatile const int*)&st->flag) return;   // every CTA sees the flag now
+    // column scans: warp w of CTA q takes digits d = q*NW + w, + ntiles*NW, ...;
+    // lane l holds tiles 5l .. 5l+4 (ntiles <= 160), all loads issued at once
+    for (int d = tile * NW + warp; d < bins; d += ntiles * NW) {
+      int* col = cnt + (size_t)d * ntiles;
+      int v[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) v[k] = 5 * lane + k < ntiles ? __ldcg(col + 5 * lane + k) : 0;
+      const int mine = v[0] + v[1] + v[2] + v[3] + v[4];
+      int x = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      int run = x - mine;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        if (5 * lane + k < ntiles) col[5 * lane + k] = run;
+        run += v[k];
+      }
+      if (lane == 31) tot[d] = x;
+    }
+    grid_barrier(&st->arrivals);
+    SORT_MARK(4 + 6 * p);
+    {   // digit bases (exclusive over digits of the totals) + this tile's column prefix
+      const int v = tid < bins ? __ldcg(tot + tid) : 0;
+      int all;
+      const int ex = block_excl_scan(v, ws, &all);
+      if (tid < bins) tpref[tid] = ex + __ldcg(cnt + (size_t)tid * ntiles + tile);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      const int64_t e = base + j * 32 + lane;
+      if (e < n) {
+        const int dig = ((unsigned)keys[j] >> shift) & (bins - 1);
+        const int loc = tstart[dig] + whist[warp * bins + dig] + lrank[j];
+        skey[loc] = keys[j];
+        sval[loc] = vals[j];
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int i = tid; i < tcnt; i += kSortThreads) {
+      const int k = skey[i];
+      const int dig = ((unsigned)k >> shift) & (bins - 1);
+      const int pos = tpref[dig] + (i - tstart[dig]);
+      kout[pos] = k;
+      vout[pos] = sval[i];
+    }
+    SORT_MARK(5 + 6 * p);
+    if (p + 1 < passes) grid_barrier(&st->arrivals);
+    SORT_MARK(6 + 6 * p);
+  }
+}
+
 // ------------------------------------------------------------------ segmented reduction
 template <int VEC>
 __device__ __forceinline__ void load_row(const float* __restrict__ src, int cols, int lane, float* v) {
@@ -618,6 +775,7 @@ static const AtCfg kAtCfgs[] = {
     {512, 2048, 4096, 110 * 1024, (const void*)sc_atomic_coop<512, 2048, 4096>},
 };
 static const int g_at_cfg = 0;
+static bool g_sort_coop_ok = false;   // sc_sort_coop fits 1 CTA/SM (scatter_prepare)
 static int g_at_blocks_per_sm = 0;   // sc_atomic_coop occupancy (scatter_prepare)
 static size_t at_fixed(const AtCfg& c) { return sizeof(int) * (2 * c.hash + c.tile) + sizeof(short) * c.tile; }
 static int at_amax(const AtCfg& c, int cols) {   // accumulator rows that fit
@@ -645,7 +803,7 @@ ScatterPlan scatter_plan(int64_t rows, int cols, int64_t n, int num_sms) {
   pl.off_status = take(sizeof(ScatterStatus));
   pl.zero_bytes = o;   // only the status block is reset per call
   pl.off_hist = take(sizeof(int) * pl.bins * pl.ntiles);   // digit-major tile counts
-  pl.off_ctr = take(sizeof(int) * kScanBlocks);
+  pl.off_ctr = take(sizeof(int) * (kScanBlocks > 1024 ? kScanBlocks : 1024));   // scan partials / digit totals
   pl.off_lookback = take(16);
   pl.off_ka = take(sizeof(int) * n);
   pl.off_va = take(sizeof(int) * n);
@@ -719,6 +877,17 @@ cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t ro
   const int m = (int)(pl.bins * pl.ntiles);
   const int32_t* kin = I;
   const int32_t* vin = nullptr;
+  if (pl.ntiles <= pl.num_sms && pl.bins <= kSortThreads && g_sort_coop_ok) {
+    int ntl = (int)pl.ntiles, passes = pl.passes, bits = pl.bits;
+    int* tot = bsum;
+    void* args[] = {(void*)&I, (void*)&ka, (void*)&va, (void*)&kb, (void*)&vb, (void*)&n, (void*)&passes,
+                    (void*)&bits, (void*)&rows, (void*)&counts, (void*)&tot, (void*)&st};
+    e = cudaLaunchCooperativeKernel((const void*)sc_sort_coop, ntl, kSortThreads, args, smd, s);
+    if (e != cudaSuccess) return e;
+    *launches += 1;
+    kin = ((pl.passes - 1) & 1) ? kb : ka;   // the last pass's output
+    vin = ((pl.passes - 1) & 1) ? vb : va;
+  } else
   for (int p = 0; p < pl.passes; ++p) {
     int32_t* ko = (p & 1) ? kb : ka;
     int32_t* vo = (p & 1) ? vb : va;
@@ -757,6 +926,13 @@ cudaError_t scatter_prepare(int bins) {
   cudaError_t e = cudaFuncSetAttribute(sc_downsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)downsweep_smem(bins));
   if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sc_sort_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)downsweep_smem(bins));
+  if (e == cudaSuccess) {
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sc_sort_coop, kSortThreads, downsweep_smem(bins));
+    g_sort_coop_ok = e == cudaSuccess && b >= 1;
+  }
+  if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sc_upsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(int) * (kSortThreads / 32) * bins));
   for (const AtCfg& c : kAtCfgs)
@@ -772,3 +948,9 @@ cudaError_t scatter_prepare(int bins) {
 }
 
 }  // namespace pg
+
+#ifdef PG_TRACE
+extern "C" int pg_debug_sort_trace(unsigned long long* out) {   // [160][16] globaltimer stamps
+  return (int)cudaMemcpyFromSymbol(out, pg::g_sort_tr, sizeof(pg::g_sort_tr));
+}
+#endif
