@@ -67,15 +67,23 @@ typedef enum {
  * conflict policy unstated; SPEC.md:111-115 names both). */
 enum {
   PG_SCATTER_DET = 0,    /* sort by row, fixed-order segmented sums: bit-reproducible */
-  PG_SCATTER_ATOMIC = 1  /* pre-aggregated red.global.add.v4.f32 (FTZ, order varies) */
+  PG_SCATTER_ATOMIC = 1  /* repeated rows pre-summed per tile, then vector atomic adds
+                            (red.global.add.v4.f32: FTZ, order varies run to run) */
 };
 
 /* pg_set_option keys */
 enum {
   PG_OPT_SCATTER = 1, /* value: PG_SCATTER_DET (default) or PG_SCATTER_ATOMIC */
   PG_OPT_STREAM = 2,  /* value: (int64_t)(cudaStream_t); 0 = legacy default stream */
-  PG_OPT_FUSED = 3    /* 1 (default): one persistent cooperative kernel per step;
+  PG_OPT_FUSED = 3,   /* 1 (default): one persistent cooperative kernel per step;
                          0: two ordinary kernels (phase 1 | phase 2), same results */
+  PG_OPT_RESERVE = 4, /* value: batch size; allocates the step workspace for it now
+                         (so later steps at <= that batch never allocate -- e.g.
+                         before CUDA-graph capture).  PG_EINVAL unless 1..2^30. */
+  PG_OPT_TRACE = 5    /* value: (int64_t) device pointer to >= 32*P uint64 slots, 0 = off.
+                         Per-CTA %globaltimer stamps of the step's stages; honoured
+                         only by the instrumented build libpg_trace.so (-DPG_TRACE),
+                         ignored by libpg.so.  For scripts/trace_step.py. */
 };
 
 /* pg_init -- allocate a model on the current CUDA device and initialise it:
@@ -134,8 +142,10 @@ pg_status pg_sync(pg_model* m);
  * W [rows][cols], Y [n][cols] fp32 and I [n] int32 are DEVICE pointers.
  * mode PG_SCATTER_DET: stable radix sort of (I[k], k), then segmented sums in
  * k order within fixed-size chunks, chunk partials combined in chunk order:
- * bit-reproducible run to run.  mode PG_SCATTER_ATOMIC: tile-local
- * pre-aggregation then red.global.add.v4.f32 (cols % 4 == 0 required).
+ * bit-reproducible run to run (cols in {1..32, 64, 128}).  mode
+ * PG_SCATTER_ATOMIC: rows repeated inside a 2048-entry tile are summed in
+ * shared memory first, everything reaches W through red.global.add.v4.f32
+ * (cols % 4 == 0, cols <= 128; other widths use scalar atomics).
  * n == 0 is a no-op.  Out-of-range I[k] -> PG_ERANGE and W unchanged.
  * stream: a cudaStream_t (NULL = legacy default).  Blocking (it reports the
  * index check); see pg_scatter_add_async for the graph-capturable variant. */

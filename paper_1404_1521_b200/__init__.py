@@ -25,7 +25,7 @@ LIB_PATH = os.path.join(_HERE, "libpg_trace.so" if os.environ.get("PG_LIB_VARIAN
 
 PG_OK, PG_EINVAL, PG_ERANGE, PG_ENOMEM, PG_ECUDA, PG_ENCCL, PG_EDIVERGED = range(7)
 PG_SCATTER_DET, PG_SCATTER_ATOMIC = 0, 1
-PG_OPT_SCATTER, PG_OPT_STREAM, PG_OPT_FUSED, PG_OPT_RESERVE = 1, 2, 3, 4
+PG_OPT_SCATTER, PG_OPT_STREAM, PG_OPT_FUSED, PG_OPT_RESERVE, PG_OPT_TRACE = 1, 2, 3, 4, 5
 
 EXPORTED = [
     "pg_init", "pg_train_step", "pg_train_step_loss", "pg_score", "pg_free", "pg_last_error",

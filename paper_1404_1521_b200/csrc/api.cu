@@ -346,10 +346,10 @@ extern "C" pg_status pg_set_option(pg_model* m, int key, int64_t value) {
     case PG_OPT_FUSED:
       m->fused = value ? 1 : 0;
       return PG_OK;
-    case 5:    // PG_OPT_TRACE (internal): device buffer of [P][16] u64 phase stamps, 0 = off
+    case PG_OPT_TRACE:   // device buffer of [P][32] u64 stage stamps (libpg_trace.so), 0 = off
       m->trace = reinterpret_cast<unsigned long long*>(value);
       return PG_OK;
-    case 4: {  // PG_OPT_RESERVE (internal): pre-size workspace for a batch
+    case PG_OPT_RESERVE: {   // pre-size the workspace for a batch
       if (value < 1 || value > (1 << 30)) return fail(PG_EINVAL, "reserve: bad batch");
       if (pg_status s = set_device(m)) return s;
       return ensure_ws(m, (int)value);
