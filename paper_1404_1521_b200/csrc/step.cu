@@ -413,6 +413,62 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
   for (int u = 0; u < 16; ++u) dacc[u] = make_float2(0.f, 0.f);
   float acc_db1 = 0.f, acc_dw2 = 0.f, acc_hinge = 0.f;
 
+  // ---- per-CTA dense partial record (after the last chunk's backward, before
+  // its aggregation, so the stores drain while the aggregation runs)
+  auto write_record = [&]() {
+    float* rec = p.dense_part + (size_t)blockIdx.x * p.dense_stride;
+    float* dsm = sig;   // [DB][32][33]: the corrupt-centre warps' dW1 rows
+    if (slot == n) {
+  #pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        dsm[(blk * 32 + lane) * 33 + 2 * u] = dacc[u].x;
+        dsm[(blk * 32 + lane) * 33 + 2 * u + 1] = dacc[u].y;
+      }
+    }
+    red[warp * 32 + lane] = acc_db1;
+    red[32 * 32 + warp * 32 + lane] = acc_dw2;
+    if (lane == 0) hinge_s[warp] = acc_hinge;
+    __syncthreads();
+    if (slot < n) {
+      if (slot == c) {
+  #pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          dacc[u].x += dsm[(blk * 32 + lane) * 33 + 2 * u];
+          dacc[u].y += dsm[(blk * 32 + lane) * 33 + 2 * u + 1];
+        }
+      }
+      float* tile = reinterpret_cast<float*>(sm + lay.wsm) + (size_t)warp * 32 * 33;   // W1 tile is dead now
+  #pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        tile[lane * 33 + 2 * u] = dacc[u].x;
+        tile[lane * 33 + 2 * u + 1] = dacc[u].y;
+      }
+      __syncwarp();
+      float4* dst = reinterpret_cast<float4*>(rec + (size_t)wrow0 * 32);
+  #pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int t = 4 * (lane + 32 * k), rr = t >> 5, cc = t & 31;
+        dst[lane + 32 * k] = make_float4(tile[rr * 33 + cc], tile[rr * 33 + cc + 1], tile[rr * 33 + cc + 2],
+                                         tile[rr * 33 + cc + 3]);
+      }
+    }
+    const int ndh = n * d * 32;
+    if (tid < 32) {
+      float a = 0.f, b = 0.f;
+      #pragma unroll 1
+      for (int w = 0; w < NW; ++w) { a += red[w * 32 + tid]; b += red[32 * 32 + w * 32 + tid]; }
+      rec[ndh + tid] = a;
+      rec[ndh + 32 + tid] = b;
+    }
+    if (tid == 32) {
+      float hsum = 0.f;
+      #pragma unroll 1
+      for (int w = 0; w < NW; ++w) hsum += hinge_s[w];
+      rec[ndh + 64] = hsum;
+    }
+    if (tid >= 64 && tid < 64 + (p.dense_stride - ndh - 65)) rec[ndh + 65 + (tid - 64)] = 0.f;
+  };
+  const int rlast = (int)((hi - lo - 1) / T);   // last non-empty chunk
 #pragma unroll 1
   for (int r = 0; r < p.R; ++r) {
     const long long e0 = lo + (long long)r * T;
@@ -561,62 +617,10 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
     }
     __syncthreads();
     if (r == 0) trace_mark(p, 4);
+    if (r == rlast) write_record();
     aggregate_chunk(p, L, cnt * (n + 1), rows_s, Gs, sm);
     if (r == 0) trace_mark(p, 5);
   }
-  // ---- per-CTA dense partial record: dW1 | db1 | dw2 | hinge, written with
-  // coalesced stores (each warp's 32 W1 rows are contiguous in the record)
-  float* rec = p.dense_part + (size_t)blockIdx.x * p.dense_stride;
-  float* dsm = sig;   // [DB][32][33]: the corrupt-centre warps' dW1 rows
-  if (slot == n) {
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      dsm[(blk * 32 + lane) * 33 + 2 * u] = dacc[u].x;
-      dsm[(blk * 32 + lane) * 33 + 2 * u + 1] = dacc[u].y;
-    }
-  }
-  red[warp * 32 + lane] = acc_db1;
-  red[32 * 32 + warp * 32 + lane] = acc_dw2;
-  if (lane == 0) hinge_s[warp] = acc_hinge;
-  __syncthreads();
-  if (slot < n) {
-    if (slot == c) {
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        dacc[u].x += dsm[(blk * 32 + lane) * 33 + 2 * u];
-        dacc[u].y += dsm[(blk * 32 + lane) * 33 + 2 * u + 1];
-      }
-    }
-    float* tile = X + (size_t)warp * 32 * 33;   // X|pg are free: warp-private transpose tile
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      tile[lane * 33 + 2 * u] = dacc[u].x;
-      tile[lane * 33 + 2 * u + 1] = dacc[u].y;
-    }
-    __syncwarp();
-    float4* dst = reinterpret_cast<float4*>(rec + (size_t)wrow0 * 32);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int t = 4 * (lane + 32 * k), rr = t >> 5, cc = t & 31;
-      dst[lane + 32 * k] = make_float4(tile[rr * 33 + cc], tile[rr * 33 + cc + 1], tile[rr * 33 + cc + 2],
-                                       tile[rr * 33 + cc + 3]);
-    }
-  }
-  const int ndh = n * d * 32;
-  if (tid < 32) {
-    float a = 0.f, b = 0.f;
-    #pragma unroll 1
-    for (int w = 0; w < NW; ++w) { a += red[w * 32 + tid]; b += red[32 * 32 + w * 32 + tid]; }
-    rec[ndh + tid] = a;
-    rec[ndh + 32 + tid] = b;
-  }
-  if (tid == 32) {
-    float hsum = 0.f;
-    #pragma unroll 1
-    for (int w = 0; w < NW; ++w) hsum += hinge_s[w];
-    rec[ndh + 64] = hsum;
-  }
-  if (tid >= 64 && tid < 64 + (p.dense_stride - ndh - 65)) rec[ndh + 65 + (tid - 64)] = 0.f;
 }
 
 // ------------------------------------------------------------------ GENERIC phase 1
