@@ -623,6 +623,211 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
   }
 }
 
+// ------------------------------------------------------------------ TILED phase 1
+// d % 32 == 0, h % 32 == 0, 64 <= h <= 128 (the large config: d = h = 128):
+// chunks of kTT = 16 examples, 384 threads, every FMA an FFMA2 with one operand
+// broadcast, W1 read from L2 once per chunk per product (no per-thread
+// redundancy), all other operands from shared memory.
+//   forward  : thread (slot s, hidden pair) accumulates 16 examples over d
+//              (x from XT[s][j][0..15] as float4 broadcasts);
+//   hinge    : warp per example, lanes over h;
+//   G rows   : thread (slot s, feature j) accumulates 16 examples over h
+//              (its W1 row, sigma/delta/delta' as [u][e] float4 broadcasts);
+//   dW1      : thread (row, 32 hidden) accumulates over the 16 examples and
+//              adds into this CTA's dense record (CTA-private, chunk order).
+constexpr int kTT = 16;
+__device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
+  const Layout& lay = p.lay;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  const int d = p.d, n = p.n, h = p.h, E = n + 1, c = n >> 1, H2 = h >> 1;
+  float* X = reinterpret_cast<float*>(sm + lay.xs);     // deduped rows [u][d]
+  float* part = X;                                      // forward partials [E][T][h]
+  float* Gs = X;                                        // gradient rows [T][E][d]
+  float* XT = reinterpret_cast<float*>(sm + lay.xt);    // [E][d][T]
+  float* SU = reinterpret_cast<float*>(sm + lay.sigu);  // [3][h][T]
+  float* SE = reinterpret_cast<float*>(sm + lay.sige);  // [3][T][h]
+  float* DW = reinterpret_cast<float*>(sm + lay.dwt);   // [T][h]
+  float* hinge_s = reinterpret_cast<float*>(sm + lay.hinge);
+  int* rows_s = reinterpret_cast<int*>(sm + lay.rows);
+  const int* pu = reinterpret_cast<const int*>(sm + lay.pu);
+  float* rec = p.dense_part + (size_t)blockIdx.x * p.dense_stride;
+  const int ndh = n * d * h;
+  const float b2 = __ldg(p.b2);
+  const long long lo = (long long)(((unsigned long long)blockIdx.x * (unsigned)p.B) / (unsigned)p.P);
+  const long long hi = (long long)(((unsigned long long)(blockIdx.x + 1) * (unsigned)p.B) / (unsigned)p.P);
+  float db1_acc = 0.f, dw2_acc = 0.f, hinge_acc = 0.f;   // thread u < h: db1[u], dw2[u]; thread 0: hinge
+#pragma unroll 1
+  for (int r = 0; r < p.R; ++r) {
+    const long long e0 = lo + (long long)r * kTT;
+    const int cnt = (int)(hi - e0 < kTT ? (hi - e0 > 0 ? hi - e0 : 0) : kTT);
+    const int L = blockIdx.x * p.R + r;
+    if (cnt <= 0) { write_empty_list(p, L); continue; }
+    gather_rows(p, sm, e0, cnt, X, rows_s, r == 0, [] {}, [] {});
+    // XT[s][j][e] = x of example e, slot s (slot n = corrupt centre); 0 past cnt
+#pragma unroll 1
+    for (int i = tid; i < E * d * kTT; i += NT) {
+      const int e = i % kTT, j = (i / kTT) % d, sl = i / (kTT * d);
+      XT[i] = e < cnt ? X[(size_t)pu[e * E + sl] * d + j] : 0.f;
+    }
+    __syncthreads();
+    if (r == 0) trace_mark(p, 1);
+    // ---- forward partials part[s][e][u]
+#pragma unroll 1
+    for (int it = tid; it < E * H2; it += NT) {
+      const int sl = it / H2, pp = it - sl * H2, ws = sl == n ? c : sl;
+      const float2* wc = reinterpret_cast<const float2*>(p.W1 + (size_t)ws * d * h) + pp;
+      const float4* xt = reinterpret_cast<const float4*>(XT + (size_t)sl * d * kTT);
+      float2 acc[kTT];
+#pragma unroll
+      for (int e = 0; e < kTT; ++e) acc[e] = make_float2(0.f, 0.f);
+#pragma unroll 4
+      for (int j = 0; j < d; ++j) {
+        const float2 w = __ldg(wc + (size_t)j * H2);
+#pragma unroll
+        for (int q = 0; q < kTT / 4; ++q) {
+          const float4 x = xt[j * (kTT / 4) + q];
+          acc[4 * q] = __ffma2_rn(w, make_float2(x.x, x.x), acc[4 * q]);
+          acc[4 * q + 1] = __ffma2_rn(w, make_float2(x.y, x.y), acc[4 * q + 1]);
+          acc[4 * q + 2] = __ffma2_rn(w, make_float2(x.z, x.z), acc[4 * q + 2]);
+          acc[4 * q + 3] = __ffma2_rn(w, make_float2(x.w, x.w), acc[4 * q + 3]);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < kTT; ++e) reinterpret_cast<float2*>(part + ((size_t)sl * kTT + e) * h)[pp] = acc[e];
+    }
+    __syncthreads();
+    if (r == 0) trace_mark(p, 2);
+    // ---- hinge, delta, delta', sigma: warp per example, lanes over h (<= 4 per lane)
+#pragma unroll 1
+    for (int e = warp; e < kTT; e += NW) {
+      float a[4], ac[4], w2v[4];
+      float sp = 0.f, spc = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int u = lane + 32 * k;
+        a[k] = ac[k] = w2v[k] = 0.f;
+        if (u < h) {
+          float ctx = __ldg(p.b1 + u);
+          for (int sl = 0; sl < n; ++sl)
+            if (sl != c) ctx += part[((size_t)sl * kTT + e) * h + u];
+          a[k] = ctx + part[((size_t)c * kTT + e) * h + u];
+          ac[k] = ctx + part[((size_t)n * kTT + e) * h + u];
+          w2v[k] = __ldg(p.w2 + u);
+          sp += w2v[k] * fminf(fmaxf(a[k], -1.f), 1.f);
+          spc += w2v[k] * fminf(fmaxf(ac[k], -1.f), 1.f);
+        }
+      }
+      sp = warp_sum(sp);
+      spc = warp_sum(spc);
+      const float m = 1.f - (sp + b2) + (spc + b2);
+      const bool active = e < cnt && m > 0.f;
+      const float g = active ? -p.inv_B : 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int u = lane + 32 * k;
+        if (u < h) {
+          const float dl = fabsf(a[k]) < 1.f ? g * w2v[k] : 0.f;
+          const float dlc = fabsf(ac[k]) < 1.f ? -g * w2v[k] : 0.f;
+          const float z = fminf(fmaxf(a[k], -1.f), 1.f), zc = fminf(fmaxf(ac[k], -1.f), 1.f);
+          SU[((size_t)0 * h + u) * kTT + e] = dl + dlc;
+          SU[((size_t)1 * h + u) * kTT + e] = dl;
+          SU[((size_t)2 * h + u) * kTT + e] = dlc;
+          SE[((size_t)0 * kTT + e) * h + u] = dl + dlc;
+          SE[((size_t)1 * kTT + e) * h + u] = dl;
+          SE[((size_t)2 * kTT + e) * h + u] = dlc;
+          DW[(size_t)e * h + u] = g * z + (-g) * zc;
+        }
+      }
+      if (lane == 0) hinge_s[e] = active ? m : 0.f;
+    }
+    __syncthreads();
+    if (r == 0) trace_mark(p, 3);
+    if (tid < h) {   // db1 / dw2 in example order
+      for (int e = 0; e < cnt; ++e) { db1_acc += SE[(size_t)e * h + tid]; dw2_acc += DW[(size_t)e * h + tid]; }
+    }
+    if (tid == 0)
+      for (int e = 0; e < cnt; ++e) hinge_acc += hinge_s[e];
+    // ---- gradient rows G[e][s][j] = sum_u W1[ws*d+j][u] * cls_s[e][u]
+#pragma unroll 1
+    for (int it = tid; it < E * d; it += NT) {
+      const int sl = it / d, j = it - sl * d, ws = sl == n ? c : sl;
+      const int cls = sl == c ? 1 : (sl == n ? 2 : 0);
+      const float4* wr = reinterpret_cast<const float4*>(p.W1 + ((size_t)ws * d + j) * h);
+      const float4* su = reinterpret_cast<const float4*>(SU + (size_t)cls * h * kTT);
+      float2 acc[kTT / 2];
+#pragma unroll
+      for (int q = 0; q < kTT / 2; ++q) acc[q] = make_float2(0.f, 0.f);
+#pragma unroll 2
+      for (int u4 = 0; u4 < h / 4; ++u4) {
+        const float4 w = __ldg(wr + u4);
+        const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int uu = 0; uu < 4; ++uu) {
+          const float2 wp = make_float2(wv[uu], wv[uu]);
+#pragma unroll
+          for (int q = 0; q < kTT / 4; ++q) {
+            const float4 sv = su[(4 * u4 + uu) * (kTT / 4) + q];
+            acc[2 * q] = __ffma2_rn(make_float2(sv.x, sv.y), wp, acc[2 * q]);
+            acc[2 * q + 1] = __ffma2_rn(make_float2(sv.z, sv.w), wp, acc[2 * q + 1]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kTT / 2; ++q) {
+        Gs[((size_t)(2 * q) * E + sl) * d + j] = acc[q].x;
+        Gs[((size_t)(2 * q + 1) * E + sl) * d + j] = acc[q].y;
+      }
+    }
+    // ---- dW1 rows (CTA record, chunk order): row rw = s*d + j, 32 hidden per item
+    const bool first = r == 0;
+#pragma unroll 1
+    for (int it = tid; it < n * d * (h / 32); it += NT) {
+      const int rw = it / (h / 32), ub = it - rw * (h / 32), sl = rw / d, j = rw - sl * d;
+      float2 acc[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] = make_float2(0.f, 0.f);
+      const int passes = sl == c ? 2 : 1;   // centre block: x_c (delta) then x'_c (delta')
+#pragma unroll 1
+      for (int ps = 0; ps < passes; ++ps) {
+        const int xs = ps == 0 ? sl : n, cls = sl == c ? (ps == 0 ? 1 : 2) : 0;
+        const float* xt = XT + ((size_t)xs * d + j) * kTT;
+#pragma unroll 1
+        for (int e = 0; e < cnt; ++e) {
+          const float xe = xt[e];
+          const float2 xp = make_float2(xe, xe);
+          const float4* se = reinterpret_cast<const float4*>(SE + ((size_t)cls * kTT + e) * h + ub * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 v = se[q];
+            acc[2 * q] = __ffma2_rn(make_float2(v.x, v.y), xp, acc[2 * q]);
+            acc[2 * q + 1] = __ffma2_rn(make_float2(v.z, v.w), xp, acc[2 * q + 1]);
+          }
+        }
+      }
+      float4* dst = reinterpret_cast<float4*>(rec + (size_t)rw * h + ub * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 o = make_float4(acc[2 * q].x, acc[2 * q].y, acc[2 * q + 1].x, acc[2 * q + 1].y);
+        if (!first) {
+          const float4 prev = __ldcg(dst + q);
+          o = make_float4(prev.x + o.x, prev.y + o.y, prev.z + o.z, prev.w + o.w);
+        }
+        dst[q] = o;
+      }
+    }
+    __syncthreads();
+    if (r == 0) trace_mark(p, 4);
+    aggregate_chunk(p, L, cnt * E, rows_s, Gs, sm);
+    if (r == 0) trace_mark(p, 5);
+  }
+  if (tid < h) {
+    rec[ndh + tid] = db1_acc;
+    rec[ndh + h + tid] = dw2_acc;
+  }
+  if (tid == 0) rec[ndh + 2 * h] = hinge_acc;
+  if (tid >= 32 && tid < 32 + (p.dense_stride - ndh - 2 * h - 1)) rec[ndh + 2 * h + 1 + (tid - 32)] = 0.f;
+}
+
 // ------------------------------------------------------------------ GENERIC phase 1
 // Any (d, n, h) with h <= 128: plain per-thread loops, W1 read through L1.
 __device__ void phase1_generic(const StepParams& p, unsigned char* sm) {
@@ -1390,7 +1595,7 @@ __device__ void build_record(const StepParams& p, unsigned char* sm) {
 }
 
 // ------------------------------------------------------------------ kernels
-template <bool FAST>
+template <int PATH>   // 0 generic, 1 fast (h == 32), 2 tiled
 __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + p.lay.mbar);
@@ -1404,7 +1609,8 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
   trace_mark(p, 0);
   trace_clock(p, 12);
   if (phases & 1) {
-    if (FAST) phase1_fast(p, smem);
+    if (PATH == 1) phase1_fast(p, smem);
+    else if (PATH == 2) phase1_tiled(p, smem);
     else phase1_generic(p, smem);
     __syncthreads();
     trace_mark(p, 6);
@@ -1428,15 +1634,19 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
 
 int step_fast_ok(int d, int n, int h) {
   const int nw = (n + 1) * (d / 32);
-  return h == 32 && d % 32 == 0 && d >= 32 && nw >= 8 && nw <= 12 && (n + 1) * kTMax <= kMaxKeys;
+  if (h == 32 && d % 32 == 0 && d >= 32 && nw >= 8 && nw <= 12 && (n + 1) * kTMax <= kMaxKeys) return 1;
+  if (d % 32 == 0 && h % 32 == 0 && h >= 64 && h <= 128 && (n + 1) * kTT <= kMaxKeys && (n + 1) * kTT <= 384)
+    return 2;
+  return 0;
 }
 
 int step_block_threads(int d, int n, int h, int fast) {
-  if (fast) return (n + 1) * (d / 32) * 32;  // 256..384 (step_fast_ok)
+  if (fast == 1) return (n + 1) * (d / 32) * 32;  // 256..384 (step_fast_ok)
   return 384;
 }
 
 int step_chunk_T(int d, int n, int h, int fast) {
+  if (fast == 2) return kTT;
   int T = kTMax;
   while ((n + 1) * T > kMaxKeys) --T;
   if (!fast) {
@@ -1445,9 +1655,13 @@ int step_chunk_T(int d, int n, int h, int fast) {
   return T;
 }
 
+static const void* step_fn(int fast) {
+  return fast == 1 ? (const void*)step_kernel<1> : fast == 2 ? (const void*)step_kernel<2> : (const void*)step_kernel<0>;
+}
+
 // Allow up to the opt-in maximum minus the kernel's static shared memory.
 cudaError_t step_prepare(int fast, size_t optin, size_t* usable) {
-  const void* fn = fast ? (const void*)step_kernel<true> : (const void*)step_kernel<false>;
+  const void* fn = step_fn(fast);
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, fn);
   if (e != cudaSuccess) return e;
@@ -1458,7 +1672,7 @@ cudaError_t step_prepare(int fast, size_t optin, size_t* usable) {
 
 void launch_step_phases(const StepParams& p, int phases, int fast, cudaStream_t s, int* launches) {
   const int NT = step_block_threads(p.d, p.n, p.h, fast);
-  void* fn = fast ? (void*)step_kernel<true> : (void*)step_kernel<false>;
+  const void* fn = step_fn(fast);
   void* args[] = {(void*)&p, (void*)&phases};
   if ((phases & 1) && (phases & 6)) cudaLaunchCooperativeKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
   else cudaLaunchKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
@@ -1468,7 +1682,7 @@ void launch_step_phases(const StepParams& p, int phases, int fast, cudaStream_t 
 void launch_step(const StepParams& p, int fused, int fast, cudaStream_t s, int* launches) {
   const int NT = step_block_threads(p.d, p.n, p.h, fast);
   const size_t smem = (size_t)p.smem_bytes;
-  void* fn = fast ? (void*)step_kernel<true> : (void*)step_kernel<false>;
+  const void* fn = step_fn(fast);
   if (fused) {
     int phases = 3;
     void* args[] = {(void*)&p, (void*)&phases};

@@ -44,6 +44,7 @@ struct Layout {
   int xs, pg, sig, gz, hinge, rows, ws, red, wsm, mbar;
   int ahk, ahc, aslot, ocnt, ocur, hj, ecnt, eoff, ecur, spos, misc, amask, pu, urow, uslot;   // chunk aggregation
   int A, Ac, SIG, DEL, DELc;   // generic path
+  int xt, sigu, sige, dwt;      // tiled path
   // phase 2
   int lbase, loff, keys, seg, stage, stagefb, carry, dred, ws2;
   int esrc, erow, hkey, hfirst, heads, hlist, rcnt, roff, rcur, misc2, rmask;
@@ -60,12 +61,22 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.mbar = 0;   // three mbarriers (phase-1 gathers, phase-2 staging, C prefetch), never aliased
   int o = 32;
   const int NW = NT / 32;
-  if (fast) {
+  if (fast == 1) {
     L.xs = o;    o = align16(o + NW * T * 32 * 4);
     L.pg = o;    o = align16(o + NW * T * 32 * 4);     // == T*(n+1)*d floats
     const int sigf = 3 * T * 32 > (d / 32) * 32 * 33 ? 3 * T * 32 : (d / 32) * 32 * 33;
     L.sig = o;   o = align16(o + sigf * 4);
     L.wsm = o;   o = align16(o + NW * 32 * 33 * 4);    // per-warp W1 transpose tile (padded)
+  } else if (fast == 2) {   // tiled path (h % 32 == 0, 64 <= h <= 128)
+    const int K = (n + 1) * T;
+    int a = K * d;                                     // deduped rows, then part [E][T][h], then G [T][E][d]
+    if ((n + 1) * T * h > a) a = (n + 1) * T * h;
+    L.xs = o;    o = align16(o + a * 4);
+    L.pg = L.xs;
+    L.xt = o;    o = align16(o + (n + 1) * d * T * 4);   // X transposed [E][d][T]
+    L.sigu = o;  o = align16(o + 3 * h * T * 4);          // sigma|delta|delta' [3][h][T]
+    L.sige = o;  o = align16(o + 3 * T * h * 4);          // the same as [3][T][h]
+    L.dwt = o;   o = align16(o + T * h * 4);              // dw2 terms [T][h]
   } else {
     L.xs = o;    o = align16(o + T * (n + 1) * d * 4); // X, later G rows
     L.pg = L.xs;
