@@ -80,7 +80,7 @@ enum {
   PG_OPT_RESERVE = 4, /* value: batch size; allocates the step workspace for it now
                          (so later steps at <= that batch never allocate -- e.g.
                          before CUDA-graph capture).  PG_EINVAL unless 1..2^30. */
-  PG_OPT_TRACE = 5    /* value: (int64_t) device pointer to >= 32*P uint64 slots, 0 = off.
+  PG_OPT_TRACE = 5    /* value: (int64_t) device pointer to >= 64*P uint64 slots, 0 = off.
                          Per-CTA %globaltimer stamps of the step's stages; honoured
                          only by the instrumented build libpg_trace.so (-DPG_TRACE),
                          ignored by libpg.so.  For scripts/trace_step.py. */

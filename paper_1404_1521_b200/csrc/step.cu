@@ -52,11 +52,11 @@ __device__ __forceinline__ void trace_mark(const StepParams& p, int k) {
   if (threadIdx.x == 0 && p.trace != nullptr) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[blockIdx.x * 32 + k] = t;
+    p.trace[blockIdx.x * 64 + k] = t;
   }
 }
 __device__ __forceinline__ void trace_clock(const StepParams& p, int k) {
-  if (threadIdx.x == 0 && p.trace != nullptr) p.trace[blockIdx.x * 32 + k] = clock64();
+  if (threadIdx.x == 0 && p.trace != nullptr) p.trace[blockIdx.x * 64 + k] = clock64();
 }
 #else
 __device__ __forceinline__ void trace_mark(const StepParams&, int) {}
@@ -636,6 +636,7 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
 //   dW1      : thread (row, 32 hidden) accumulates over the 16 examples and
 //              adds into this CTA's dense record (CTA-private, chunk order).
 constexpr int kTT = 16;
+constexpr int kXTS = 20;   // XT row stride (floats): 16 examples + 4 pad, 16 B aligned
 __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
   const Layout& lay = p.lay;
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
@@ -663,29 +664,32 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
     const int L = blockIdx.x * p.R + r;
     if (cnt <= 0) { write_empty_list(p, L); continue; }
     gather_rows(p, sm, e0, cnt, X, rows_s, r == 0, [] {}, [] {});
-    // XT[s][j][e] = x of example e, slot s (slot n = corrupt centre); 0 past cnt
+    // XT[s][j][e] = x of example e, slot s (slot n = corrupt centre); 0 past cnt.
+    // Warp per (s, e), lanes over j: conflict-free row reads; the [j][e] rows are
+    // kXTS floats apart so the column writes are 4-way at worst.
 #pragma unroll 1
-    for (int i = tid; i < E * d * kTT; i += NT) {
-      const int e = i % kTT, j = (i / kTT) % d, sl = i / (kTT * d);
-      XT[i] = e < cnt ? X[(size_t)pu[e * E + sl] * d + j] : 0.f;
+    for (int se = warp; se < E * kTT; se += NW) {
+      const int sl = se / kTT, e = se - sl * kTT;
+      const float* xr = X + (size_t)(e < cnt ? pu[e * E + sl] : 0) * d;
+      for (int j = lane; j < d; j += 32) XT[((size_t)sl * d + j) * kXTS + e] = e < cnt ? xr[j] : 0.f;
     }
     __syncthreads();
-    if (r == 0) trace_mark(p, 1);
+    if (r < 2) trace_mark(p, 1 + 32 * r);
     // ---- forward partials part[s][e][u]
 #pragma unroll 1
     for (int it = tid; it < E * H2; it += NT) {
       const int sl = it / H2, pp = it - sl * H2, ws = sl == n ? c : sl;
       const float2* wc = reinterpret_cast<const float2*>(p.W1 + (size_t)ws * d * h) + pp;
-      const float4* xt = reinterpret_cast<const float4*>(XT + (size_t)sl * d * kTT);
+      const float4* xt = reinterpret_cast<const float4*>(XT + (size_t)sl * d * kXTS);
       float2 acc[kTT];
 #pragma unroll
       for (int e = 0; e < kTT; ++e) acc[e] = make_float2(0.f, 0.f);
-#pragma unroll 4
+#pragma unroll 8
       for (int j = 0; j < d; ++j) {
         const float2 w = __ldg(wc + (size_t)j * H2);
 #pragma unroll
         for (int q = 0; q < kTT / 4; ++q) {
-          const float4 x = xt[j * (kTT / 4) + q];
+          const float4 x = xt[j * (kXTS / 4) + q];
           acc[4 * q] = __ffma2_rn(w, make_float2(x.x, x.x), acc[4 * q]);
           acc[4 * q + 1] = __ffma2_rn(w, make_float2(x.y, x.y), acc[4 * q + 1]);
           acc[4 * q + 2] = __ffma2_rn(w, make_float2(x.z, x.z), acc[4 * q + 2]);
@@ -696,7 +700,7 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
       for (int e = 0; e < kTT; ++e) reinterpret_cast<float2*>(part + ((size_t)sl * kTT + e) * h)[pp] = acc[e];
     }
     __syncthreads();
-    if (r == 0) trace_mark(p, 2);
+    if (r < 2) trace_mark(p, 2 + 32 * r);
     // ---- hinge, delta, delta', sigma: warp per example, lanes over h (<= 4 per lane)
 #pragma unroll 1
     for (int e = warp; e < kTT; e += NW) {
@@ -729,9 +733,9 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
           const float dl = fabsf(a[k]) < 1.f ? g * w2v[k] : 0.f;
           const float dlc = fabsf(ac[k]) < 1.f ? -g * w2v[k] : 0.f;
           const float z = fminf(fmaxf(a[k], -1.f), 1.f), zc = fminf(fmaxf(ac[k], -1.f), 1.f);
-          SU[((size_t)0 * h + u) * kTT + e] = dl + dlc;
-          SU[((size_t)1 * h + u) * kTT + e] = dl;
-          SU[((size_t)2 * h + u) * kTT + e] = dlc;
+          SU[((size_t)0 * h + u) * kXTS + e] = dl + dlc;
+          SU[((size_t)1 * h + u) * kXTS + e] = dl;
+          SU[((size_t)2 * h + u) * kXTS + e] = dlc;
           SE[((size_t)0 * kTT + e) * h + u] = dl + dlc;
           SE[((size_t)1 * kTT + e) * h + u] = dl;
           SE[((size_t)2 * kTT + e) * h + u] = dlc;
@@ -741,23 +745,25 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
       if (lane == 0) hinge_s[e] = active ? m : 0.f;
     }
     __syncthreads();
-    if (r == 0) trace_mark(p, 3);
+    if (r < 2) trace_mark(p, 3 + 32 * r);
     if (tid < h) {   // db1 / dw2 in example order
       for (int e = 0; e < cnt; ++e) { db1_acc += SE[(size_t)e * h + tid]; dw2_acc += DW[(size_t)e * h + tid]; }
     }
     if (tid == 0)
       for (int e = 0; e < cnt; ++e) hinge_acc += hinge_s[e];
-    // ---- gradient rows G[e][s][j] = sum_u W1[ws*d+j][u] * cls_s[e][u]
+    // ---- gradient rows G[e][s][j] = sum_u W1[ws*d+j][u] * cls_s[e][u]: thread per
+    // row (lanes over consecutive j of one slot -> the sigma/delta reads are
+    // broadcasts), W1 row streamed as float4 (4 in flight)
 #pragma unroll 1
     for (int it = tid; it < E * d; it += NT) {
       const int sl = it / d, j = it - sl * d, ws = sl == n ? c : sl;
       const int cls = sl == c ? 1 : (sl == n ? 2 : 0);
       const float4* wr = reinterpret_cast<const float4*>(p.W1 + ((size_t)ws * d + j) * h);
-      const float4* su = reinterpret_cast<const float4*>(SU + (size_t)cls * h * kTT);
+      const float4* su = reinterpret_cast<const float4*>(SU + (size_t)cls * h * kXTS);
       float2 acc[kTT / 2];
 #pragma unroll
       for (int q = 0; q < kTT / 2; ++q) acc[q] = make_float2(0.f, 0.f);
-#pragma unroll 2
+#pragma unroll 4
       for (int u4 = 0; u4 < h / 4; ++u4) {
         const float4 w = __ldg(wr + u4);
         const float wv[4] = {w.x, w.y, w.z, w.w};
@@ -766,7 +772,7 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
           const float2 wp = make_float2(wv[uu], wv[uu]);
 #pragma unroll
           for (int q = 0; q < kTT / 4; ++q) {
-            const float4 sv = su[(4 * u4 + uu) * (kTT / 4) + q];
+            const float4 sv = su[(4 * u4 + uu) * (kXTS / 4) + q];
             acc[2 * q] = __ffma2_rn(make_float2(sv.x, sv.y), wp, acc[2 * q]);
             acc[2 * q + 1] = __ffma2_rn(make_float2(sv.z, sv.w), wp, acc[2 * q + 1]);
           }
@@ -778,47 +784,89 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
         Gs[((size_t)(2 * q + 1) * E + sl) * d + j] = acc[q].y;
       }
     }
-    // ---- dW1 rows (CTA record, chunk order): row rw = s*d + j, 32 hidden per item
-    const bool first = r == 0;
-#pragma unroll 1
-    for (int it = tid; it < n * d * (h / 32); it += NT) {
-      const int rw = it / (h / 32), ub = it - rw * (h / 32), sl = rw / d, j = rw - sl * d;
-      float2 acc[16];
+    if (r < 2) trace_mark(p, 27 + 32 * r);
+    // ---- dW1 rows into this CTA's record (chunk order): warp per row, lane =
+    // 4 hidden units; the class's 16 x 4 sigma/delta values sit in registers
+    // across rows, x[e] of the row is a float4 broadcast, the record row is
+    // read (later chunks) and written as one coalesced 512 B access, with LA
+    // record rows of reads in flight.  Centre rows add x'_c * delta' (delta'
+    // read from shared memory) before their single write.
+    {
+      const bool first = r == 0;
+      const int u0 = 4 * lane;
+      const bool has_u = u0 < h;
+      const int nA = n * d;
+      int cur_cls = -1;
+      float2 sreg[kTT][2];
+      constexpr int LA = 4;   // record-row lookahead
+      float4 pre[LA];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) acc[q] = make_float2(0.f, 0.f);
-      const int passes = sl == c ? 2 : 1;   // centre block: x_c (delta) then x'_c (delta')
+      for (int k = 0; k < LA; ++k) {
+        const int rr = warp + k * NW;
+        pre[k] = (rr < nA && has_u && !first) ? __ldcg(reinterpret_cast<const float4*>(rec + (size_t)rr * h) + lane)
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll 1
-      for (int ps = 0; ps < passes; ++ps) {
-        const int xs = ps == 0 ? sl : n, cls = sl == c ? (ps == 0 ? 1 : 2) : 0;
-        const float* xt = XT + ((size_t)xs * d + j) * kTT;
-#pragma unroll 1
-        for (int e = 0; e < cnt; ++e) {
-          const float xe = xt[e];
-          const float2 xp = make_float2(xe, xe);
-          const float4* se = reinterpret_cast<const float4*>(SE + ((size_t)cls * kTT + e) * h + ub * 32);
+      for (int rr = warp; rr < nA; rr += NW) {
+        const int sl = rr / d, j = rr - sl * d;
+        const int cls = sl == c ? 1 : 0;
+        if (cls != cur_cls) {
+          cur_cls = cls;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 v = se[q];
-            acc[2 * q] = __ffma2_rn(make_float2(v.x, v.y), xp, acc[2 * q]);
-            acc[2 * q + 1] = __ffma2_rn(make_float2(v.z, v.w), xp, acc[2 * q + 1]);
+          for (int e = 0; e < kTT; ++e) {
+            const float4 v = has_u ? *reinterpret_cast<const float4*>(SE + ((size_t)cls * kTT + e) * h + u0)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            sreg[e][0] = make_float2(v.x, v.y);
+            sreg[e][1] = make_float2(v.z, v.w);
           }
         }
-      }
-      float4* dst = reinterpret_cast<float4*>(rec + (size_t)rw * h + ub * 32);
+        const float4* xt4 = reinterpret_cast<const float4*>(XT + ((size_t)sl * d + j) * kXTS);
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float4 o = make_float4(acc[2 * q].x, acc[2 * q].y, acc[2 * q + 1].x, acc[2 * q + 1].y);
-        if (!first) {
-          const float4 prev = __ldcg(dst + q);
-          o = make_float4(prev.x + o.x, prev.y + o.y, prev.z + o.z, prev.w + o.w);
+        for (int q = 0; q < kTT / 4; ++q) {
+          const float4 x = xt4[q];
+          const float xe[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float2 xp = make_float2(xe[t], xe[t]);
+            a0 = __ffma2_rn(sreg[4 * q + t][0], xp, a0);
+            a1 = __ffma2_rn(sreg[4 * q + t][1], xp, a1);
+          }
         }
-        dst[q] = o;
+        if (cls == 1 && has_u) {   // centre block: + x'_c * delta'
+          const float4* xc4 = reinterpret_cast<const float4*>(XT + ((size_t)n * d + j) * kXTS);
+#pragma unroll
+          for (int q = 0; q < kTT / 4; ++q) {
+            const float4 x = xc4[q];
+            const float xe[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float4 v = *reinterpret_cast<const float4*>(SE + ((size_t)2 * kTT + 4 * q + t) * h + u0);
+              const float2 xp = make_float2(xe[t], xe[t]);
+              a0 = __ffma2_rn(make_float2(v.x, v.y), xp, a0);
+              a1 = __ffma2_rn(make_float2(v.z, v.w), xp, a1);
+            }
+          }
+        }
+        const float4 prev = pre[0];
+#pragma unroll
+        for (int t = 0; t + 1 < LA; ++t) pre[t] = pre[t + 1];
+        {
+          const int rn = rr + LA * NW;
+          pre[LA - 1] = (rn < nA && has_u && !first) ? __ldcg(reinterpret_cast<const float4*>(rec + (size_t)rn * h) + lane)
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (has_u) {
+          const float4 o = make_float4(a0.x, a0.y, a1.x, a1.y);
+          reinterpret_cast<float4*>(rec + (size_t)rr * h)[lane] =
+              first ? o : make_float4(prev.x + o.x, prev.y + o.y, prev.z + o.z, prev.w + o.w);
+        }
       }
     }
     __syncthreads();
-    if (r == 0) trace_mark(p, 4);
+    if (r < 2) trace_mark(p, 4 + 32 * r);
     aggregate_chunk(p, L, cnt * E, rows_s, Gs, sm);
-    if (r == 0) trace_mark(p, 5);
+    if (r < 2) trace_mark(p, 5 + 32 * r);
   }
   if (tid < h) {
     rec[ndh + tid] = db1_acc;
@@ -1499,7 +1547,7 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
   if (p.mode == 0) M = det_counts(p, sm, pre_a, pre_b);   // contains __syncthreads
   trace_mark(p, 30);
 #ifdef PG_TRACE
-  if (tid == 0 && p.trace != nullptr) p.trace[blockIdx.x * 32 + 31] = M;
+  if (tid == 0 && p.trace != nullptr) p.trace[blockIdx.x * 64 + 31] = M;
 #endif
   __syncthreads();
   const float loss = s_loss;

@@ -73,8 +73,8 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
     if ((n + 1) * T * h > a) a = (n + 1) * T * h;
     L.xs = o;    o = align16(o + a * 4);
     L.pg = L.xs;
-    L.xt = o;    o = align16(o + (n + 1) * d * T * 4);   // X transposed [E][d][T]
-    L.sigu = o;  o = align16(o + 3 * h * T * 4);          // sigma|delta|delta' [3][h][T]
+    L.xt = o;    o = align16(o + (n + 1) * d * (T + 4) * 4);   // X transposed [E][d][T + 4 pad]
+    L.sigu = o;  o = align16(o + 3 * h * (T + 4) * 4);    // sigma|delta|delta' [3][h][T + 4 pad]
     L.sige = o;  o = align16(o + 3 * T * h * 4);          // the same as [3][T][h]
     L.dwt = o;   o = align16(o + T * h * 4);              // dw2 terms [T][h]
   } else {

@@ -15,8 +15,9 @@ ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--split", action="store_true")
 ap.add_argument("--atomic", action="store_true")
 ap.add_argument("--scatter-bench", action="store_true")
+ap.add_argument("--large", action="store_true", help="V 1M, d 128, n 5, h 128 (tiled path)")
 a = ap.parse_args()
-V, d, n, h = 100_000, 64, 5, 32
+V, d, n, h = (1_000_000, 128, 5, 128) if a.large else (100_000, 64, 5, 32)
 if a.scatter_bench:
     I, Y = synth.scatter_inputs(V, d, 1_000_000, "zipf", "random")
     W = torch.zeros(V, d, device="cuda")

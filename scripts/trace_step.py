@@ -18,11 +18,12 @@ ap.add_argument("--split", action="store_true")
 ap.add_argument("--atomic", action="store_true")
 ap.add_argument("--flush", action="store_true")
 ap.add_argument("--busy", action="store_true", help="keep the GPU busy between steps (no host sync)")
+ap.add_argument("--large", action="store_true", help="V 1M, d 128, n 5, h 128 (tiled path)")
 a = ap.parse_args()
-V, d, n, h = 100_000, 64, 5, 32
+V, d, n, h = (1_000_000, 128, 5, 128) if a.large else (100_000, 64, 5, 32)
 m = pg.PolyglotModel(V, d, n, h, fused=not a.split, scatter=1 if a.atomic else 0)
 P = min(148, a.batch)
-tr = torch.zeros(a.steps, 160 * 32, dtype=torch.int64, device="cuda")
+tr = torch.zeros(a.steps, 160 * 64, dtype=torch.int64, device="cuda")
 bs = [synth.batch(V, n, a.batch, seed=1, step=t) for t in range(a.steps)]
 di = [torch.from_numpy(i).cuda() for i, _ in bs]
 dc = [torch.from_numpy(c).cuda() for _, c in bs]
@@ -38,7 +39,7 @@ torch.cuda.synchronize()
 names = ["start", "gathered", "fwd", "sigma", "bwd", "agg", "p1end", "barrier", "p2head", "dense", "", "end",
          "", "", "agg.ins", "agg.scan", "agg.place", "agg.acc", "agg.csr", "idx",
          "m.esrc", "m.trip2", "m.hash", "m.scan", "m.trip3", "g.rows", "w1", "s.loaded", "s.shfl", "p2.dense_ld", "p2.counts"]
-X = tr.view(a.steps, 160, 32).cpu().numpy()[2:, :P].astype(np.float64)
+X = tr.view(a.steps, 160, 64).cpu().numpy()[2:, :P].astype(np.float64)
 rel = []
 mhz = []
 for x in X:
@@ -69,3 +70,8 @@ for b in slow:
     print(f"  {b:4d} {ends[b]:6.2f} {int(x[b, 31]):4d} | " + " ".join(f"{v:5.2f}" for v in st))
 med = np.median(X[-1][:, 31])
 print(f"median M {med:.0f}, max M {X[-1][:, 31].max():.0f}")
+
+if a.large:   # tiled path, second chunk (slots 32 + k)
+    for k, nm in ((33, "c2.xt"), (34, "c2.fwd"), (35, "c2.sigma"), (59, "c2.G"), (36, "c2.dW1"), (37, "c2.agg")):
+        col = A2 = (X[:, :, k] - X[:, :, 0].min(axis=1, keepdims=True)) / 1e3
+        print(f"  {nm:9s} med {np.nanmedian(col):7.2f}  max {np.nanmean(np.nanmax(col, axis=1)):7.2f}")
