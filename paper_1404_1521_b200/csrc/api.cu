@@ -52,6 +52,7 @@ struct pg_model {
   int64_t V = 0;
   int d = 0, n = 0, h = 0;
   float *C = nullptr, *W1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;
+  float* W1T = nullptr;   // tiled path: W1 transposed [h][n*d]
   DevStatus* st = nullptr;
   DevStatus* st_host = nullptr;  // pinned mirror for blocking reads
   cudaStream_t stream = nullptr;
@@ -102,6 +103,15 @@ __global__ void init_uniform_kernel(float* out, int64_t count, unsigned long lon
 }
 
 // ------------------------------------------------------------------ score kernel
+// W1T[u][r] = W1[r][u] (the tiled step path reads W1 rows along u as columns).
+__global__ void transpose_w1_kernel(const float* __restrict__ W1, float* __restrict__ W1T, int rows, int h) {
+  const int64_t total = (int64_t)rows * h;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(i / rows), r = (int)(i % rows);
+    W1T[i] = W1[(size_t)r * h + u];
+  }
+}
+
 // Warp per window: s = w2 . clamp(W1^T x + b1, -1, 1) + b2.
 __global__ void score_kernel(const float* __restrict__ C, const float* __restrict__ W1,
                              const float* __restrict__ b1, const float* __restrict__ w2,
@@ -293,6 +303,14 @@ extern "C" pg_status pg_init(pg_model** out, int64_t vocab, int32_t dim, int32_t
   init_uniform_kernel<<<blocks, 256>>>(m->W1, nW, seed, 1, 0.5 / (double)(window * dim));
   init_uniform_kernel<<<1, 256>>>(m->w2, hidden, seed, 2, 0.5 / (double)hidden);
   m->launches += 3;
+  if (m->fast == 2) {
+    if (cudaMalloc(&m->W1T, sizeof(float) * nW) != cudaSuccess) {
+      cudaGetLastError();
+      return bail(fail(PG_ENOMEM, "pg_init: allocation failed (W1T)"));
+    }
+    transpose_w1_kernel<<<blocks, 256>>>(m->W1, m->W1T, window * dim, hidden);
+    m->launches += 1;
+  }
   cudaMemset(m->b1, 0, sizeof(float) * hidden);
   cudaMemset(m->b2, 0, sizeof(float));
   DevStatus z{};
@@ -315,7 +333,7 @@ extern "C" void pg_free(pg_model* m) {
   else cudaDeviceSynchronize();
   if (m->comm) nccl_shim_destroy(m->comm);
   free_ws(m);
-  cudaFree(m->C); cudaFree(m->W1); cudaFree(m->b1); cudaFree(m->w2); cudaFree(m->b2);
+  cudaFree(m->C); cudaFree(m->W1); cudaFree(m->W1T); cudaFree(m->b1); cudaFree(m->w2); cudaFree(m->b2);
   cudaFree(m->st); cudaFreeHost(m->st_host);
   cudaFree(m->d_idx); cudaFree(m->d_corr); cudaFree(m->d_scores);
   free_dp(m);
@@ -389,6 +407,11 @@ extern "C" pg_status pg_set_params(pg_model* m, const float* C, const float* W1,
   pg_status s = PG_OK;
   if (C && !s) s = copy_param(m->C, C, sizeof(float) * (size_t)m->V * m->d, m->stream);
   if (W1 && !s) s = copy_param(m->W1, W1, sizeof(float) * nW, m->stream);
+  if (W1 && !s && m->W1T) {
+    transpose_w1_kernel<<<m->num_sms * 8, 256, 0, m->stream>>>(m->W1, m->W1T, m->n * m->d, m->h);
+    m->launches += 1;
+    CU(cudaGetLastError());
+  }
   if (b1 && !s) s = copy_param(m->b1, b1, sizeof(float) * m->h, m->stream);
   if (w2 && !s) s = copy_param(m->w2, w2, sizeof(float) * m->h, m->stream);
   if (!std::isnan(b2) && !s) {
@@ -499,7 +522,7 @@ extern "C" pg_status pg_sync(pg_model* m) {
 static StepParams make_params(pg_model* m, const Geometry& g, const int32_t* idx, const int32_t* corr, int B,
                               float lr, float* loss_dev) {
   StepParams p{};
-  p.C = m->C; p.W1 = m->W1; p.b1 = m->b1; p.w2 = m->w2; p.b2 = m->b2;
+  p.C = m->C; p.W1 = m->W1; p.W1T = m->W1T; p.b1 = m->b1; p.w2 = m->w2; p.b2 = m->b2;
   p.V = m->V; p.d = m->d; p.n = m->n; p.h = m->h;
   p.idx = idx; p.corr = corr; p.B = B;
   p.inv_B = 1.0f / (float)((int64_t)B * m->world);

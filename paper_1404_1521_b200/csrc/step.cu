@@ -752,36 +752,36 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
     if (tid == 0)
       for (int e = 0; e < cnt; ++e) hinge_acc += hinge_s[e];
     // ---- gradient rows G[e][s][j] = sum_u W1[ws*d+j][u] * cls_s[e][u]: thread per
-    // row (lanes over consecutive j of one slot -> the sigma/delta reads are
-    // broadcasts), W1 row streamed as float4 (4 in flight)
+    // row, lanes over consecutive j of one slot, so W1 is read from its
+    // transposed mirror W1T[u][row] as coalesced 128 B lines and the
+    // sigma/delta reads are broadcasts; 8 u per trip in flight
+    {
+      const int nd = n * d;
 #pragma unroll 1
-    for (int it = tid; it < E * d; it += NT) {
-      const int sl = it / d, j = it - sl * d, ws = sl == n ? c : sl;
-      const int cls = sl == c ? 1 : (sl == n ? 2 : 0);
-      const float4* wr = reinterpret_cast<const float4*>(p.W1 + ((size_t)ws * d + j) * h);
-      const float4* su = reinterpret_cast<const float4*>(SU + (size_t)cls * h * kXTS);
-      float2 acc[kTT / 2];
+      for (int it = tid; it < E * d; it += NT) {
+        const int sl = it / d, j = it - sl * d, ws = sl == n ? c : sl;
+        const int cls = sl == c ? 1 : (sl == n ? 2 : 0);
+        const float* wt = p.W1T + (size_t)ws * d + j;   // + u * nd
+        const float4* su = reinterpret_cast<const float4*>(SU + (size_t)cls * h * kXTS);
+        float2 acc[kTT / 2];
 #pragma unroll
-      for (int q = 0; q < kTT / 2; ++q) acc[q] = make_float2(0.f, 0.f);
-#pragma unroll 4
-      for (int u4 = 0; u4 < h / 4; ++u4) {
-        const float4 w = __ldg(wr + u4);
-        const float wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int uu = 0; uu < 4; ++uu) {
-          const float2 wp = make_float2(wv[uu], wv[uu]);
+        for (int q = 0; q < kTT / 2; ++q) acc[q] = make_float2(0.f, 0.f);
+#pragma unroll 8
+        for (int u = 0; u < h; ++u) {
+          const float w = __ldg(wt + (size_t)u * nd);
+          const float2 wp = make_float2(w, w);
 #pragma unroll
           for (int q = 0; q < kTT / 4; ++q) {
-            const float4 sv = su[(4 * u4 + uu) * (kXTS / 4) + q];
+            const float4 sv = su[u * (kXTS / 4) + q];
             acc[2 * q] = __ffma2_rn(make_float2(sv.x, sv.y), wp, acc[2 * q]);
             acc[2 * q + 1] = __ffma2_rn(make_float2(sv.z, sv.w), wp, acc[2 * q + 1]);
           }
         }
-      }
 #pragma unroll
-      for (int q = 0; q < kTT / 2; ++q) {
-        Gs[((size_t)(2 * q) * E + sl) * d + j] = acc[q].x;
-        Gs[((size_t)(2 * q + 1) * E + sl) * d + j] = acc[q].y;
+        for (int q = 0; q < kTT / 2; ++q) {
+          Gs[((size_t)(2 * q) * E + sl) * d + j] = acc[q].x;
+          Gs[((size_t)(2 * q + 1) * E + sl) * d + j] = acc[q].y;
+        }
       }
     }
     if (r < 2) trace_mark(p, 27 + 32 * r);
@@ -1087,6 +1087,11 @@ __device__ __forceinline__ void dense_apply(const StepParams& p, unsigned char* 
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           if (base + k < DL) q[k] = cur[k] - p.lr * sv[k];
+        if (p.W1T != nullptr && base < ndh) {   // tiled path: keep W1^T in step
+          const int row = base / p.h, u = base - row * p.h, nd = p.n * p.d;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) p.W1T[(size_t)(u + k) * nd + row] = cur[k] - p.lr * sv[k];
+        }
       } else {
 #pragma unroll 1
         for (int k = 0; k < 4; ++k)

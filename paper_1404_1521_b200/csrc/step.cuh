@@ -155,6 +155,7 @@ struct StepParams {
   // parameters
   float* C;
   float* W1;
+  float* W1T;        // tiled path: W1 transposed [h][n*d], kept in step by the dense update (else null)
   float* b1;
   float* w2;
   const float* b2;
