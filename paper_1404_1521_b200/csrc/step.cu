@@ -675,7 +675,7 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
     }
     __syncthreads();
     if (r < 2) trace_mark(p, 1 + 32 * r);
-    // ---- forward partials part[s][e][u]
+    // ---- forward partials part[s][e][u]: thread (slot, hidden pair), 16 examples
 #pragma unroll 1
     for (int it = tid; it < E * H2; it += NT) {
       const int sl = it / H2, pp = it - sl * H2, ws = sl == n ? c : sl;
@@ -752,36 +752,40 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
     if (tid == 0)
       for (int e = 0; e < cnt; ++e) hinge_acc += hinge_s[e];
     // ---- gradient rows G[e][s][j] = sum_u W1[ws*d+j][u] * cls_s[e][u]: thread per
-    // row, lanes over consecutive j of one slot, so W1 is read from its
-    // transposed mirror W1T[u][row] as coalesced 128 B lines and the
-    // sigma/delta reads are broadcasts; 8 u per trip in flight
+    // two rows (j, j + d/2) of one slot, lanes over consecutive j, so W1 is read
+    // from its transposed mirror W1T[u][row] as coalesced 128 B lines and the
+    // sigma/delta float4 broadcasts serve both rows
     {
-      const int nd = n * d;
+      const int nd = n * d, D2 = d >> 1;
 #pragma unroll 1
-      for (int it = tid; it < E * d; it += NT) {
-        const int sl = it / d, j = it - sl * d, ws = sl == n ? c : sl;
+      for (int it = tid; it < E * D2; it += NT) {
+        const int sl = it / D2, j = it - sl * D2, ws = sl == n ? c : sl;
         const int cls = sl == c ? 1 : (sl == n ? 2 : 0);
-        const float* wt = p.W1T + (size_t)ws * d + j;   // + u * nd
+        const float* wt = p.W1T + (size_t)ws * d + j;   // rows j and j + D2, + u * nd
         const float4* su = reinterpret_cast<const float4*>(SU + (size_t)cls * h * kXTS);
-        float2 acc[kTT / 2];
+        float2 acc[2][kTT / 2];
 #pragma unroll
-        for (int q = 0; q < kTT / 2; ++q) acc[q] = make_float2(0.f, 0.f);
-#pragma unroll 8
+        for (int q = 0; q < kTT / 2; ++q) acc[0][q] = acc[1][q] = make_float2(0.f, 0.f);
+#pragma unroll 4
         for (int u = 0; u < h; ++u) {
-          const float w = __ldg(wt + (size_t)u * nd);
-          const float2 wp = make_float2(w, w);
+          const float w0 = __ldg(wt + (size_t)u * nd), w1 = __ldg(wt + (size_t)u * nd + D2);
 #pragma unroll
           for (int q = 0; q < kTT / 4; ++q) {
             const float4 sv = su[u * (kXTS / 4) + q];
-            acc[2 * q] = __ffma2_rn(make_float2(sv.x, sv.y), wp, acc[2 * q]);
-            acc[2 * q + 1] = __ffma2_rn(make_float2(sv.z, sv.w), wp, acc[2 * q + 1]);
+            const float2 lo = make_float2(sv.x, sv.y), hi = make_float2(sv.z, sv.w);
+            acc[0][2 * q] = __ffma2_rn(lo, make_float2(w0, w0), acc[0][2 * q]);
+            acc[0][2 * q + 1] = __ffma2_rn(hi, make_float2(w0, w0), acc[0][2 * q + 1]);
+            acc[1][2 * q] = __ffma2_rn(lo, make_float2(w1, w1), acc[1][2 * q]);
+            acc[1][2 * q + 1] = __ffma2_rn(hi, make_float2(w1, w1), acc[1][2 * q + 1]);
           }
         }
 #pragma unroll
-        for (int q = 0; q < kTT / 2; ++q) {
-          Gs[((size_t)(2 * q) * E + sl) * d + j] = acc[q].x;
-          Gs[((size_t)(2 * q + 1) * E + sl) * d + j] = acc[q].y;
-        }
+        for (int rr2 = 0; rr2 < 2; ++rr2)
+#pragma unroll
+          for (int q = 0; q < kTT / 2; ++q) {
+            Gs[((size_t)(2 * q) * E + sl) * d + j + rr2 * D2] = acc[rr2][q].x;
+            Gs[((size_t)(2 * q + 1) * E + sl) * d + j + rr2 * D2] = acc[rr2][q].y;
+          }
       }
     }
     if (r < 2) trace_mark(p, 27 + 32 * r);
