@@ -368,6 +368,37 @@ def run_extras(pg, torch, synth, np, dev, stream, flush, model):
                                               "algorithmic_bytes": alg_bytes, "unique_rows": U}
     res["scatter_microbench"] = {"config": "100k x 64 fp32 table, 1M rows, L2 flushed, W[I]+=Y (pg_scatter_add)",
                                  "peak_hbm_gbs": hbm, "results": sc}
+    # BASELINE.json configs[3] shape (V 1M, d 128, n 5, h 128) on this GPU: the
+    # tiled phase-1 path; per-GPU batch 512 (global 4096 over 8 GPUs) and 4096
+    Vl, dl, nl, hl = 1_000_000, 128, 5, 128
+    big = pg.PolyglotModel(Vl, dl, nl, hl, seed=42, stream=stream)
+    lg = {}
+    peak = fp32_alu_peak_tflops(peaks.get("sm_max_mhz", 1965.0))
+    for B in (512, 4096):
+        big.reserve(B)
+        bs = [synth.batch(Vl, nl, B, seed=11, step=t) for t in range(8)]
+        di = [torch.from_numpy(i).to(dev) for i, _ in bs]
+        dc = [torch.from_numpy(c).to(dev) for _, c in bs]
+        with torch.cuda.stream(stream):
+            for t in range(3):
+                big.train_step(di[t], dc[t], 0.1, loss_out=None)
+            torch.cuda.synchronize()
+            tms = []
+            for t in range(3, 8):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                big.train_step(di[t], dc[t], 0.1, loss_out=None)
+                b.record(stream)
+                tms.append((a, b))
+            torch.cuda.synchronize()
+        us = 1e3 * statistics.mean([a.elapsed_time(b) for a, b in tms])
+        tf = 2.0 * FMA_PER_EXAMPLE(dl, nl, hl) * B / (us * 1e-6) / 1e12
+        lg[str(B)] = {"us_per_step": us, "examples_per_s": B / (us * 1e-6), "tflops": tf, "frac_of_fp32_peak": tf / peak}
+    big.sync()
+    big.close()
+    res["large_config"] = {"config": "V 1M, d 128, n 5, h 128 (BASELINE.json configs[3] shape), L2 flushed, 1 GPU",
+                           "path": "tiled phase 1 (FFMA2)", "results": lg}
     return res
 
 

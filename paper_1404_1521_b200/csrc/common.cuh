@@ -43,7 +43,8 @@ __device__ __forceinline__ float4 ldcg4(const float* p) {
 // arrival value `old` names the instance (old / G) and its release point
 // ((old / G + 1) * G).  Waiters poll the counter itself -- one L2 round trip
 // after the last arrival, no separate generation word.  All users of one
-// counter must launch the same grid size.  Ordering: bar.sync makes the CTA's
+// counter must launch the same grid size (callers keep one counter per grid
+// size).  Ordering: bar.sync makes the CTA's
 // writes visible to thread 0; its acq_rel arrival RMW (cumulative) publishes
 // them; the waiter's acquire load of the final count synchronises with every
 // arrival, and bar.sync hands that on to the CTA.

@@ -1674,9 +1674,9 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
   }
   const bool prep = (phases & 2) && p.mode == 0;
   if ((phases & 1) && (phases & 6)) {
-    const unsigned long long target = grid_arrive(&p.st->bar_arrivals);
+    const unsigned long long target = grid_arrive(&p.st->bar_arrivals[gridDim.x - 1]);
     if (prep) phase2_prep(p, smem);   // overlaps the barrier
-    grid_wait(&p.st->bar_arrivals, target);
+    grid_wait(&p.st->bar_arrivals[gridDim.x - 1], target);
   } else if (prep) {
     phase2_prep(p, smem);
     __syncthreads();

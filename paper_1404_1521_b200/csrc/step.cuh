@@ -19,9 +19,10 @@ struct DevStatus {
   unsigned long long bad;        // min over (pos << 32 | uint32 value)
   int flags;                     // bit0 bad index
   int pad0[29];
-  // line 1: grid barrier -- monotonic arrival count (never reset)
-  alignas(128) unsigned long long bar_arrivals;
-  unsigned long long pad1[15];
+  // lines 1-10: grid barrier -- monotonic arrival counts (never reset), one per
+  // grid size: the barrier needs every launch that uses a counter to have the
+  // same number of CTAs, and P = min(#SMs, batch) changes with the batch
+  alignas(128) unsigned long long bar_arrivals[160];
   // line 2: phase-2 arrival counter (flag-reset protocol)
   alignas(128) unsigned done;
   unsigned pad2[31];
@@ -36,7 +37,7 @@ struct DevStatus {
   float last_loss;
   int pad3[21];
 };
-static_assert(sizeof(DevStatus) == 512, "DevStatus: four 128 B lines");
+static_assert(sizeof(DevStatus) == 3 * 128 + 160 * 8, "DevStatus layout");
 
 // Shared-memory carve-up (byte offsets), computed once on the host.
 struct Layout {

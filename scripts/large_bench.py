@@ -30,5 +30,5 @@ for B in (512, 4096):
         tms.append((a, b))
     torch.cuda.synchronize()
     us = statistics.median([a.elapsed_time(b) for a, b in tms]) * 1e3
-    fma = 3 * 2 * n * d * h + 2 * d * h   # shared-context form per example (forward, G rows, dW1)
+    fma = (n * d * h + d * h) + ((n + 1) * d * h) + ((n + 1) * d * h)   # forward (shared context), G rows, dW1
     print(f"large B={B}: {us:8.1f} us/step  {B / us * 1e6:12.0f} ex/s  {2 * fma * B / us / 1e6:6.2f} TFLOP/s")

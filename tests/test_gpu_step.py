@@ -220,3 +220,15 @@ def test_owner_overflow_sorted_fallback(pg):
     rl = [oracle.train_step(ref, idx, corr, 0.1)]
     assert_parity(np.array(gl), np.array(rl), p0, m.get_params(), ref, tau_delta=1e-4)
     m.close()
+
+
+@pytest.mark.timeout(300)
+def test_one_model_many_batch_sizes(pg):
+    # the grid size P = min(#SMs, B) changes with the batch; the fused kernel's
+    # grid barrier must stay consistent across launches of different grids
+    m = make(pg, POLY)
+    for B in (4096, 16, 4096, 7, 149, 100, 4096, 1, 2048):
+        idx, corr = synth.batch(POLY["V"], POLY["n"], B, seed=3, step=B)
+        loss = m.train_step(idx, corr, 0.1)
+        assert np.isfinite(loss)
+    m.close()
