@@ -1335,6 +1335,8 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
   const int HS = lay.HS;
   const float nlr = -p.lr;
   unsigned* rmask = reinterpret_cast<unsigned*>(sm + lay.rmask);
+  __shared__ int s_nseg;
+  if (tid == 0) s_nseg = 0;
   asm volatile("cp.async.wait_group 1;" ::: "memory");   // row ids landed (partials may still fly)
   __syncthreads();
   trace_mark(p, 21);
@@ -1411,21 +1413,74 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
     const int r = eslot[e];
     hlist[roff[r] + mask_rank<16>(rmask + r * 16, e)] = (unsigned short)e;
   }
+  // long rows (more than kLongRow partials: the Zipf head rows this CTA owns) are
+  // summed in kLongRow-entry segments by separate threads, then the segments are
+  // added in order -- a fixed association that depends only on the row's count
+  constexpr int kLongRow = 32;
+  int* rsplit = rcur;                                   // row -> first segment, -1: not split
+  int* segrow = hrid;                                   // segment -> row (-1: unused)
+  float4* lpart = reinterpret_cast<float4*>(hkey);      // [segment][Q] partial sums (hkey|hfirst)
+  const int maxseg = quad ? (2 * HS * 4) / (Q * 16) : 0;
+  int* segidx = hrid + maxseg;
+  #pragma unroll 1
+  for (int r = tid; r < nrows; r += NT) {
+    int b = -1;
+    const int m = rcnt[r];
+    if (quad && m > kLongRow) {
+      const int S = (m + kLongRow - 1) / kLongRow;
+      b = atomicAdd(&s_nseg, S);
+      const bool fits = b + S <= maxseg;
+      for (int t = 0; t < S && b + t < maxseg; ++t) { segrow[b + t] = fits ? r : -1; segidx[b + t] = t; }
+      if (!fits) b = -1;
+    }
+    rsplit[r] = b;
+  }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   trace_mark(p, 24);
+  const int nseg = s_nseg < maxseg ? s_nseg : maxseg;
   // ---- ordered sum of each distinct row's partials, one RMW of C; one thread
   // per (row, feature quad) when d % 4 == 0, else one warp per row
   if (quad) {
     const float4* S4 = reinterpret_cast<const float4*>(stage);
 #pragma unroll 1
-    for (int it = tid; it < nrows * Q; it += NT) {
-      const int ri = it / Q, q = it - ri * Q;
+    for (int it = tid; it < (nrows + nseg) * Q; it += NT) {
+      const int k = it / Q, q = it - k * Q;
+      if (k < nseg) {   // one segment of a long row
+        const int r = segrow[k];
+        if (r >= 0) {
+          const int s0 = segidx[k] * kLongRow, m = rcnt[r] - s0;
+          lpart[k * Q + q] = ordered_quadsum(S4, hlist + roff[r] + s0, m < kLongRow ? m : kLongRow, Q, q);
+        }
+        continue;
+      }
+      const int ri = k - nseg;
+      if (rsplit[ri] >= 0) continue;
       const float4 a = ordered_quadsum(S4, hlist + roff[ri], rcnt[ri], Q, q);
       if (write) {
         float4* c4 = reinterpret_cast<float4*>(p.C + (size_t)rrow[ri] * d) + q;
         const float4 o = ri < ccap ? S4[(size_t)(M + ri) * Q + q] : __ldcg(c4);
         *c4 = make_float4(o.x + nlr * a.x, o.y + nlr * a.y, o.z + nlr * a.z, o.w + nlr * a.w);
+      }
+    }
+    if (nseg > 0) {
+      __syncthreads();
+#pragma unroll 1
+      for (int it = tid; it < nseg * Q; it += NT) {   // combine each split row's segments in order
+        const int k = it / Q, q = it - k * Q;
+        const int r = segrow[k];
+        if (r < 0 || segidx[k] != 0) continue;
+        const int S = (rcnt[r] + kLongRow - 1) / kLongRow;
+        float4 a = lpart[k * Q + q];
+        for (int t = 1; t < S; ++t) {
+          const float4 v = lpart[(k + t) * Q + q];
+          a = make_float4(a.x + v.x, a.y + v.y, a.z + v.z, a.w + v.w);
+        }
+        if (write) {
+          float4* c4 = reinterpret_cast<float4*>(p.C + (size_t)rrow[r] * d) + q;
+          const float4 o = r < ccap ? S4[(size_t)(M + r) * Q + q] : __ldcg(c4);
+          *c4 = make_float4(o.x + nlr * a.x, o.y + nlr * a.y, o.z + nlr * a.z, o.w + nlr * a.w);
+        }
       }
     }
   } else {
