@@ -524,32 +524,39 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
     }
     __syncthreads();
     if (r == 0) trace_mark(p, 2);
-    // ---- sigma stage: warp per example, lane = hidden unit; two examples per
-    // pass so the two shuffle-reduction chains overlap
+    // ---- sigma stage: warp per example, lane = hidden unit; KS examples per
+    // pass (e, e + NW, e + 2 NW) so a chunk of <= KS*NW examples takes one pass
+    // and the shuffle-reduction chains overlap
+    constexpr int KS = 3;
     #pragma unroll 1
-    for (int e = warp; e < cnt; e += 2 * NW) {
-      const int e2 = e + NW;
-      const bool two = e2 < cnt;
+    for (int e = warp; e < cnt; e += KS * NW) {
+      bool has[KS];
+#pragma unroll
+      for (int k = 0; k < KS; ++k) has[k] = e + k * NW < cnt;
       // all (n+1)*DB <= 12 block partials in flight at once, then summed per
       // category in ascending block order (context | centre | corrupt centre)
-      float v0[12], v1[12];
+      float v[KS][12];
 #pragma unroll
-      for (int w = 0; w < 12; ++w) {
-        v0[w] = w < NW ? part[(w * T + e) * 32 + lane] : 0.f;
-        v1[w] = (two && w < NW) ? part[(w * T + e2) * 32 + lane] : 0.f;
-      }
-      float actx[2] = {0.f, 0.f}, acen[2] = {0.f, 0.f}, acor[2] = {0.f, 0.f};
+      for (int k = 0; k < KS; ++k)
+#pragma unroll
+        for (int w = 0; w < 12; ++w) v[k][w] = (has[k] && w < NW) ? part[(w * T + e + k * NW) * 32 + lane] : 0.f;
+      float actx[KS], acen[KS], acor[KS];
+#pragma unroll
+      for (int k = 0; k < KS; ++k) actx[k] = acen[k] = acor[k] = 0.f;
       if (r == 0 && e == 0) trace_mark(p, 27);
 #pragma unroll
       for (int w = 0; w < 12; ++w) {   // branch-free: +0.0 into the other categories is exact
         const bool cor = w >= n * DB, cen = !cor && w >= c * DB && w < (c + 1) * DB, ctx = !cor && !cen;
-        acor[0] += cor ? v0[w] : 0.f; acor[1] += cor ? v1[w] : 0.f;
-        acen[0] += cen ? v0[w] : 0.f; acen[1] += cen ? v1[w] : 0.f;
-        actx[0] += ctx ? v0[w] : 0.f; actx[1] += ctx ? v1[w] : 0.f;
-      }
-      float z[2], zc[2], a[2], ac[2], sp[2], spc[2];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < KS; ++k) {
+          acor[k] += cor ? v[k][w] : 0.f;
+          acen[k] += cen ? v[k][w] : 0.f;
+          actx[k] += ctx ? v[k][w] : 0.f;
+        }
+      }
+      float z[KS], zc[KS], a[KS], ac[KS], sp[KS], spc[KS];
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
         const float base = b1 + actx[k];
         a[k] = base + acen[k];
         ac[k] = base + acor[k];
@@ -561,16 +568,16 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < KS; ++k) {
           sp[k] += __shfl_xor_sync(0xffffffffu, sp[k], o);
           spc[k] += __shfl_xor_sync(0xffffffffu, spc[k], o);
         }
       }
       if (r == 0 && e == 0) trace_mark(p, 28);
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        if (k == 1 && !two) break;
-        const int ee = k == 0 ? e : e2;
+      for (int k = 0; k < KS; ++k) {
+        if (!has[k]) break;
+        const int ee = e + k * NW;
         const float sv = sp[k] + b2, svc = spc[k] + b2;
         const float m = 1.f - sv + svc;
         const bool active = m > 0.f;
