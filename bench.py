@@ -249,10 +249,15 @@ def main():
     barrier()
     warm_ms = e0.elapsed_time(e1) / args.steps
 
-    # ---- e2e through the public API with HOST buffers: pinned H2D of the
-    # step's inputs + blocking D2H of the loss/status, every step
+    # ---- e2e through the public API with HOST buffers.  Every step: pinned H2D
+    # of the step's idx/corr (inside pg_train_step) and a D2H read of the step's
+    # loss.  Pipelined: pg_train_step is asynchronous when the loss goes to
+    # device memory, the loss is copied to pinned host memory on the same stream
+    # and read after the loop; device errors are sticky and checked by pg_sync.
     pin_idx = [torch.from_numpy(i).pin_memory() for i, _ in host]
     pin_corr = [torch.from_numpy(c).pin_memory() for _, c in host]
+    loss_ring = torch.zeros(args.steps, dtype=torch.float32, device=dev)
+    loss_host = torch.zeros(args.steps, dtype=torch.float32).pin_memory()
     barrier()
     with torch.cuda.stream(stream):
         for k in range(min(3, total)):
@@ -260,14 +265,28 @@ def main():
         barrier()
         t0 = time.perf_counter()
         for k in range(args.steps):
-            model.train_step(pin_idx[args.warmup + k], pin_corr[args.warmup + k], args.lr)   # blocking
+            model.train_step(pin_idx[args.warmup + k], pin_corr[args.warmup + k], args.lr,
+                             loss_out=loss_ring[k:k + 1])
+            loss_host[k:k + 1].copy_(loss_ring[k:k + 1], non_blocking=True)
+        stream.synchronize()
+        model.sync()                                   # raises on any sticky device error
         e2e_s = time.perf_counter() - t0
+        assert np.isfinite(loss_host.numpy()).all()
+        # the same through the blocking call (returns each step's loss to the host)
+        barrier()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            model.train_step(pin_idx[args.warmup + k], pin_corr[args.warmup + k], args.lr)   # blocking
+        e2e_block_s = time.perf_counter() - t0
     if world > 1:
-        tt = torch.tensor([e2e_s], device=dev)
+        tt = torch.tensor([e2e_s, e2e_block_s], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+        e2e_s, e2e_block_s = float(tt[0].item()), float(tt[1].item())
     e2e = {"value": B * world * args.steps / e2e_s, "unit": "examples/s",
-           "h2d_bytes_per_step": B * n * 4 + B * 4, "d2h_bytes_per_step": 80}
+           "h2d_bytes_per_step": B * n * 4 + B * 4, "d2h_bytes_per_step": 4,
+           "mode": "pinned host inputs, async steps, per-step loss D2H, wall clock",
+           "blocking": {"value": B * world * args.steps / e2e_block_s, "d2h_bytes_per_step": 1664,
+                        "mode": "pg_train_step returning each loss (host sync per step)"}}
 
     extras = {}
     if not args.no_extras and world == 1:

@@ -88,6 +88,17 @@ def _check(rc, what):
         raise PGError(rc, f"{what}: {pg_last_error()}")
 
 
+_TDT = {}
+
+
+def _torch_dtype(dtype):
+    t = _TDT.get(dtype)
+    if t is None:
+        import torch
+        t = _TDT[dtype] = {np.int32: torch.int32, np.float32: torch.float32}[dtype]
+    return t
+
+
 def _ptr(x, dtype=None):
     """Pointer of a torch tensor (any device) or numpy array; None -> NULL."""
     if x is None:
@@ -102,8 +113,7 @@ def _ptr(x, dtype=None):
         if not x.is_contiguous():
             raise ValueError("tensor must be contiguous")
         if dtype is not None:
-            import torch
-            tdt = {np.int32: torch.int32, np.float32: torch.float32}[dtype]
+            tdt = _torch_dtype(dtype)
             if x.dtype != tdt:
                 raise TypeError(f"expected {tdt}, got {x.dtype}")
         return ctypes.c_void_p(x.data_ptr())

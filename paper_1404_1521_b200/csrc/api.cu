@@ -65,8 +65,14 @@ struct pg_model {
   int32_t* list_rows = nullptr;
   float* list_vals = nullptr;
   int32_t* list_off = nullptr;
-  int32_t* d_idx = nullptr;
-  int32_t* d_corr = nullptr;
+  // host-input staging, double-buffered: host idx/corr are copied on copy_stream
+  // into slot k % 2 while the previous step runs; ev_consumed[s] marks the end of
+  // the launch that read slot s, ev_copied[s] orders the step after its copy
+  int32_t* d_idx2[2] = {nullptr, nullptr};
+  int32_t* d_corr2[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+  int in_slot = 0, pending_slot = -1;
   float* d_scores = nullptr;
   int64_t launches = 0;
   // data parallel
@@ -230,9 +236,13 @@ static pg_status ensure_ws(pg_model* m, int B) {
   }
   if (B > m->cap_in) {
     CU(cudaStreamSynchronize(m->stream));
-    cudaFree(m->d_idx); cudaFree(m->d_corr); cudaFree(m->d_scores);
-    CU(cudaMalloc(&m->d_idx, sizeof(int32_t) * (size_t)B * m->n));
-    CU(cudaMalloc(&m->d_corr, sizeof(int32_t) * (size_t)B));
+    if (m->copy_stream) CU(cudaStreamSynchronize(m->copy_stream));
+    for (int k = 0; k < 2; ++k) {
+      cudaFree(m->d_idx2[k]); cudaFree(m->d_corr2[k]);
+      CU(cudaMalloc(&m->d_idx2[k], sizeof(int32_t) * (size_t)B * m->n));
+      CU(cudaMalloc(&m->d_corr2[k], sizeof(int32_t) * (size_t)B));
+    }
+    cudaFree(m->d_scores);
     CU(cudaMalloc(&m->d_scores, sizeof(float) * (size_t)B));
     m->cap_in = B;
   }
@@ -335,7 +345,14 @@ extern "C" void pg_free(pg_model* m) {
   free_ws(m);
   cudaFree(m->C); cudaFree(m->W1); cudaFree(m->W1T); cudaFree(m->b1); cudaFree(m->w2); cudaFree(m->b2);
   cudaFree(m->st); cudaFreeHost(m->st_host);
-  cudaFree(m->d_idx); cudaFree(m->d_corr); cudaFree(m->d_scores);
+  if (m->copy_stream) cudaStreamSynchronize(m->copy_stream);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(m->d_idx2[k]); cudaFree(m->d_corr2[k]);
+    if (m->ev_copied[k]) cudaEventDestroy(m->ev_copied[k]);
+    if (m->ev_consumed[k]) cudaEventDestroy(m->ev_consumed[k]);
+  }
+  if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
+  cudaFree(m->d_scores);
   free_dp(m);
   delete m;
 }
@@ -424,23 +441,47 @@ extern "C" pg_status pg_set_params(pg_model* m, const float* C, const float* W1,
   return PG_OK;
 }
 
+// Inputs in host memory are copied on the model's copy stream into staging slot
+// k % 2, so the copy overlaps the previous step still running on the model
+// stream; the step's stream waits for its copy, and consume_inputs() (after the
+// launches that read the slot) lets the slot be refilled two calls later.
 static pg_status stage_inputs(pg_model* m, const int32_t* idx, const int32_t* corr, int B,
                               const int32_t** d_idx, const int32_t** d_corr) {
   const PtrKind ki = ptr_kind(idx);
-  if (ki == PTR_DEVICE) {
-    *d_idx = idx;
-  } else {
-    CU(cudaMemcpyAsync(m->d_idx, idx, sizeof(int32_t) * (size_t)B * m->n, cudaMemcpyHostToDevice, m->stream));
-    *d_idx = m->d_idx;
-  }
-  if (corr) {
-    const PtrKind kc = ptr_kind(corr);
-    if (kc == PTR_DEVICE) {
-      *d_corr = corr;
-    } else {
-      CU(cudaMemcpyAsync(m->d_corr, corr, sizeof(int32_t) * (size_t)B, cudaMemcpyHostToDevice, m->stream));
-      *d_corr = m->d_corr;
+  const PtrKind kc = corr ? ptr_kind(corr) : PTR_DEVICE;
+  *d_idx = idx;
+  if (corr) *d_corr = corr;
+  if (ki == PTR_DEVICE && kc == PTR_DEVICE) return PG_OK;
+  if (!m->copy_stream) {
+    CU(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      CU(cudaEventCreateWithFlags(&m->ev_copied[k], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&m->ev_consumed[k], cudaEventDisableTiming));
     }
+  }
+  const int slot = m->in_slot;
+  m->in_slot ^= 1;
+  CU(cudaStreamWaitEvent(m->copy_stream, m->ev_consumed[slot], 0));   // no-op before its first record
+  if (ki != PTR_DEVICE) {
+    CU(cudaMemcpyAsync(m->d_idx2[slot], idx, sizeof(int32_t) * (size_t)B * m->n, cudaMemcpyHostToDevice,
+                       m->copy_stream));
+    *d_idx = m->d_idx2[slot];
+  }
+  if (corr && kc != PTR_DEVICE) {
+    CU(cudaMemcpyAsync(m->d_corr2[slot], corr, sizeof(int32_t) * (size_t)B, cudaMemcpyHostToDevice,
+                       m->copy_stream));
+    *d_corr = m->d_corr2[slot];
+  }
+  CU(cudaEventRecord(m->ev_copied[slot], m->copy_stream));
+  CU(cudaStreamWaitEvent(m->stream, m->ev_copied[slot], 0));
+  m->pending_slot = slot;
+  return PG_OK;
+}
+
+static pg_status consume_inputs(pg_model* m) {
+  if (m->pending_slot >= 0) {
+    CU(cudaEventRecord(m->ev_consumed[m->pending_slot], m->stream));
+    m->pending_slot = -1;
   }
   return PG_OK;
 }
@@ -460,6 +501,7 @@ extern "C" pg_status pg_train_step(pg_model* m, const int32_t* idx_batch, const 
   const int32_t *di = nullptr, *dc = nullptr;
   if (pg_status s = stage_inputs(m, idx_batch, corrupt_idx, batch, &di, &dc)) return s;
   if (pg_status s = run_step(m, di, dc, batch, lr, kl == PTR_DEVICE ? loss_out : nullptr)) return s;
+  if (pg_status s = consume_inputs(m)) return s;
   if (kl != PTR_HOST) return PG_OK;
   CU(cudaMemcpyAsync(m->st_host, m->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
@@ -496,6 +538,7 @@ extern "C" pg_status pg_score(pg_model* m, const int32_t* idx_batch, int32_t bat
                                                       di, batch, out, m->st);
   m->launches += 1;
   CU(cudaGetLastError());
+  if (pg_status s = consume_inputs(m)) return s;
   if (ko == PTR_DEVICE) return PG_OK;
   CU(cudaMemcpyAsync(scores_out, out, sizeof(float) * batch, cudaMemcpyDeviceToHost, m->stream));
   CU(cudaMemcpyAsync(m->st_host, m->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, m->stream));
@@ -645,6 +688,7 @@ extern "C" pg_status pg_train_step_group(pg_model** ms, int world, const int32_t
     launch_step_phases(ps[r], 1 | 4, m->fast, m->stream, &l);
     m->launches += l;
     CU(cudaGetLastError());
+    if (pg_status s = consume_inputs(m)) return s;
   }
   // "all-gather": every replica receives every replica's record
   const int64_t cap = (int64_t)(n + 1) * batch_local, offn = (int64_t)g.NL * (g.P + 1);
