@@ -232,3 +232,24 @@ def test_one_model_many_batch_sizes(pg):
         loss = m.train_step(idx, corr, 0.1)
         assert np.isfinite(loss)
     m.close()
+
+
+def test_async_host_inputs_pipeline_equals_device_inputs(pg):
+    # host (pinned and pageable) inputs are staged on a copy stream into two
+    # alternating device slots; many steps in flight must give exactly the
+    # parameters of the same steps fed from device memory
+    import torch
+    batches = [synth.batch(POLY["V"], POLY["n"], 1024, seed=21, step=t) for t in range(12)]
+    a = make(pg, POLY, seed=5)
+    b = make(pg, POLY, seed=5)
+    loss_a = torch.zeros(12, device="cuda")
+    for t, (i, c) in enumerate(batches):
+        hi = torch.from_numpy(i).pin_memory() if t % 2 == 0 else i      # pinned / pageable
+        hc = torch.from_numpy(c).pin_memory() if t % 2 == 0 else c
+        a.train_step(hi, hc, 0.1, loss_out=loss_a[t:t + 1])
+    a.sync()
+    lb = [b.train_step(torch.from_numpy(i).cuda(), torch.from_numpy(c).cuda(), 0.1) for i, c in batches]
+    assert np.array_equal(loss_a.cpu().numpy(), np.array(lb, np.float32))
+    for x, y in zip(a.get_params()[:4], b.get_params()[:4]):
+        assert np.array_equal(x, y)
+    a.close(); b.close()
