@@ -748,6 +748,7 @@ namespace {
 std::mutex g_sc_mu;
 void* g_sc_ws[16] = {nullptr};
 size_t g_sc_cap[16] = {0};
+unsigned long long g_sc_epoch[16] = {0};
 }
 
 static pg_status scatter_common(float* W, int64_t rows, int32_t cols, const float* Y, const int32_t* I, int64_t n,
@@ -757,6 +758,8 @@ static pg_status scatter_common(float* W, int64_t rows, int32_t cols, const floa
   if (mode != PG_SCATTER_DET && mode != PG_SCATTER_ATOMIC) return fail(PG_EINVAL, "pg_scatter_add: bad mode");
   if (!scatter_supported(cols, mode))
     return fail(PG_EINVAL, "pg_scatter_add: DET mode supports cols in {<=32, 64, 128} (got %d)", cols);
+  if ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(Y)) & 15)
+    return fail(PG_EINVAL, "pg_scatter_add: W and Y must be 16-byte aligned");
   if (n == 0) return PG_OK;
   if (n >= (1ll << 30)) return fail(PG_EINVAL, "pg_scatter_add: n must be < 2^30");
   if (ptr_kind(W) != PTR_DEVICE || ptr_kind(Y) != PTR_DEVICE || ptr_kind(I) != PTR_DEVICE)
@@ -774,20 +777,24 @@ static pg_status scatter_common(float* W, int64_t rows, int32_t cols, const floa
     cudaFree(g_sc_ws[dev]);
     g_sc_ws[dev] = nullptr;
     CU(cudaMalloc(&g_sc_ws[dev], pl.total_bytes));
+    CU(cudaMemset(g_sc_ws[dev], 0, pl.zero_bytes));   // status block (sc_atomic_hot never clears it per call)
     g_sc_cap[dev] = pl.total_bytes;
     CU(scatter_prepare(1024));   // the largest digit table any plan uses
   }
-  int l = 0;
-  CU(scatter_launch(pl, g_sc_ws[dev], W, rows, cols, Y, I, n, mode, s, &l));
+  int l = 0, slot = -1;
+  CU(scatter_launch(pl, g_sc_ws[dev], W, rows, cols, Y, I, n, mode, s, &l, g_sc_epoch[dev]++, &slot));
   ScatterStatus* st = reinterpret_cast<ScatterStatus*>(static_cast<unsigned char*>(g_sc_ws[dev]) + pl.off_status);
-  if (err_dev) CU(cudaMemcpyAsync(err_dev, &st->flag, sizeof(int), cudaMemcpyDeviceToDevice, s));
+  const int* flag_dev = slot < 0 ? &st->flag : &st->hot[slot].flag;
+  if (err_dev) CU(cudaMemcpyAsync(err_dev, flag_dev, sizeof(int), cudaMemcpyDeviceToDevice, s));
   if (!blocking) return PG_OK;
   ScatterStatus hs;
   CU(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
-  if (hs.flag) {
+  const int flag = slot < 0 ? hs.flag : hs.hot[slot].flag;
+  const unsigned long long bad = slot < 0 ? hs.bad : ~hs.hot[slot].nbad;
+  if (flag) {
     return fail(PG_ERANGE, "pg_scatter_add: index out of range at position %lld (value %d); W unchanged",
-                (long long)(hs.bad >> 32), (int)(unsigned)(hs.bad & 0xffffffffull));
+                (long long)(bad >> 32), (int)(unsigned)(bad & 0xffffffffull));
   }
   return PG_OK;
 }

@@ -13,8 +13,10 @@
 //   fix-up kernel combines in chunk order with a fixed-shape tree.  Every row
 //   receives exactly ONE vector reduction of its fixed-order total, so the
 //   result does not depend on timing.
-// ATOMIC: validation pass, then red.global.add.v4.f32 per 16 B of each Y row
-//   (FTZ), no ordering guarantee.
+// ATOMIC: one cooperative streaming pass (sc_atomic_hot): index check, grid
+//   barrier, frequent rows summed in shared memory, everything else reaches W
+//   by red.global.add.v4.f32 per 16 B (FTZ); no ordering
+//   guarantee.
 #include "common.cuh"
 #include "scatter.cuh"
 
@@ -624,107 +626,218 @@ __global__ void sc_validate(const int32_t* __restrict__ I, int64_t n, int64_t ro
   }
 }
 
-// Cooperative ATOMIC scatter (cols % 4 == 0, cols <= 128): one launch.
-// Every CTA first checks its grid-strided share of I; after a grid barrier all
-// CTAs see the same error flag, so a bad index still means "nothing applied".
-// Then each CTA takes kAtTile consecutive entries per round, finds the rows that
-// occur more than once in its tile (smem hash with counts), sums those rows'
-// Y entries in shared memory and flushes each with one red.global.add.v4.f32
-// per 16 B; rows seen once go straight from Y (streamed, read once) to W with
-// vector reductions.  Zipf head rows thus cost one global reduction per tile,
-// and uniform traffic stays a single streaming pass.
-template <int kAtThreads, int kAtTile, int kAtHash>
-__global__ void __launch_bounds__(kAtThreads) sc_atomic_coop(const int32_t* __restrict__ I,
-                                                             const float* __restrict__ Y, float* W,
-                                                             int64_t rows, int cols, int64_t n, int amax,
-                                                             ScatterStatus* st) {
-  constexpr int kAtAcc = 160;
-  extern __shared__ __align__(16) unsigned char at_sm[];
-  int* hk = reinterpret_cast<int*>(at_sm);                 // [kAtHash]
-  int* hc = hk + kAtHash;                                  // [kAtHash] count, then accumulator (-1: direct)
-  int* sI = hc + kAtHash;                                  // [kAtTile]
-  short* eslot = reinterpret_cast<short*>(sI + kAtTile);   // [kAtTile]
-  float* acc = reinterpret_cast<float*>(eslot + kAtTile);  // [kAtAcc][cols]
-  __shared__ int arow[kAtAcc];
-  __shared__ int nacc;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NWp = kAtThreads / 32;
+// Cooperative ATOMIC scatter, hot-set form (cols % 4 == 0, cols <= 128).
+// Plain per-16 B vector reductions stream at ~4.3 TB/s of Y on uniform
+// indices, but the L2 serialises reductions to one line (~5 ns each), so a
+// Zipf head row with 80k entries alone would take > 500 us
+// (scripts/micro/red_stream.cu, bulk_reduce.cu).  So:
+//  1. every CTA checks its grid-strided share of I (all loads issued at once)
+//     and, redundantly and identically, counts a fixed strided sample of
+//     kHotSample entries in an smem hash; rows seen >= 2 times in the sample
+//     (relative frequency >~ 0.05 %) become the CTA's hot set, most frequent
+//     first: the first ha go to tier A (a private accumulator per warp), the
+//     next up to kHotB to tier B (one shared accumulator per CTA);
+//  2. the CTA's first rows of Y are loaded, then the grid barrier (a bad index
+//     anywhere means nothing is applied);
+//  3. CTA b streams its contiguous share of entries once (Y read with
+//     evict-first loads, U rows in flight per lane group): a tier-A row is
+//     added into the warp's private accumulator (the warp's lane groups take
+//     turns, no atomics), a tier-B row with shared-memory atomics (rare
+//     collisions), every other row goes straight to W with
+//     red.global.add.v4.f32 per 16 B;
+//  4. the accumulators (tier A summed over warps in warp order) reach W with
+//     one vector reduction per 16 B per CTA.
+// Uniform indices thus stay one streaming pass, and a Zipf head row costs one
+// reduction per CTA instead of one per entry.
+constexpr int kHotSample = 4096;
+constexpr int kHotSampleHash = 8192;
+constexpr int kHotHash = 1024;
+constexpr int kHotB = 256;
+constexpr size_t kHotPrefetchMax = 48u << 20;
+template <int kThreads, int U>
+__global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __restrict__ I,
+                                                             const float* __restrict__ Y, float* W, int64_t rows,
+                                                             int cols, int64_t n, int ha, int hb,
+                                                             ScatterStatus* st, int par) {
+  constexpr int NW = kThreads / 32;
+  extern __shared__ __align__(16) unsigned char ah_sm[];
+  float* accA = reinterpret_cast<float*>(ah_sm);                                // [NW][ha][cols]
+  float* accB = accA + (size_t)NW * ha * cols;                                 // [hb][cols]
+  int* skey = reinterpret_cast<int*>(ah_sm);   // [kHotSampleHash] (aliases the accumulators)
+  int* scnt = skey + kHotSampleHash;           // [kHotSampleHash]
+  __shared__ int hkey[kHotHash], hslot[kHotHash], hrow[32 + kHotB];
+  __shared__ int nhot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q = cols >> 2;
   const int G = q >= 32 ? 32 : q, per = 32 / G, sub = lane / G, gl = lane % G;
-  for (int64_t e = (int64_t)blockIdx.x * kAtThreads + tid; e < n; e += (int64_t)gridDim.x * kAtThreads) {
-    const int key = __ldg(I + e);
-    if (key < 0 || (int64_t)key >= rows) {
-      atomicMin(&st->bad, ((unsigned long long)e << 32) | (unsigned)key);
-      atomicOr(&st->flag, 1);
+  const int64_t ns = n < kHotSample ? n : kHotSample;
+  const int64_t sstride = n / (ns > 0 ? ns : 1);
+  constexpr int kSPer = (kHotSample + kThreads - 1) / kThreads;
+  int samp[kSPer];
+#pragma unroll
+  for (int j = 0; j < kSPer; ++j) {
+    const int64_t i = (int64_t)j * kThreads + tid;
+    samp[j] = i < ns ? __ldg(I + i * sstride) : -1;
+  }
+  // W's first touch by a reduction after a cold L2 is an L2 miss the atomic
+  // unit waits on; when W is small next to the L2, pull it in while the
+  // prologue runs (this CTA's 1/gridDim share of its 128 B lines).
+  if ((size_t)rows * cols * sizeof(float) <= kHotPrefetchMax) {
+    const int64_t lines = ((int64_t)rows * cols * (int64_t)sizeof(float)) >> 7;
+    const char* wb = reinterpret_cast<const char*>(W);
+    for (int64_t l = (int64_t)blockIdx.x * kThreads + tid; l < lines; l += (int64_t)gridDim.x * kThreads)
+      asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(wb + (l << 7)));
+  }
+  {   // validation: this CTA's grid-strided share, 4 x int4 per thread per trip
+    const int64_t n4 = ((uintptr_t)I & 15) == 0 ? n >> 2 : 0;
+    const int4* I4 = reinterpret_cast<const int4*>(I);
+    for (int64_t e0 = (int64_t)blockIdx.x * kThreads + tid; e0 < n4; e0 += 4 * (int64_t)gridDim.x * kThreads) {
+      int4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t e = e0 + (int64_t)j * gridDim.x * kThreads;
+        v[j] = e < n4 ? __ldg(I4 + e) : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t e = e0 + (int64_t)j * gridDim.x * kThreads;
+        const int k4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (e < n4 && (k4[c] < 0 || (int64_t)k4[c] >= rows)) {
+            atomicMax(&st->hot[par].nbad, ~(((unsigned long long)(4 * e + c) << 32) | (unsigned)k4[c]));
+            atomicOr(&st->hot[par].flag, 1);
+          }
+      }
+    }
+    for (int64_t e = 4 * n4 + (int64_t)blockIdx.x * kThreads + tid; e < n; e += (int64_t)gridDim.x * kThreads) {
+      const int key = __ldg(I + e);
+      if (key < 0 || (int64_t)key >= rows) {
+        atomicMax(&st->hot[par].nbad, ~(((unsigned long long)e << 32) | (unsigned)key));
+        atomicOr(&st->hot[par].flag, 1);
+      }
     }
   }
-  grid_barrier(&st->arrivals);
-  if (*(volatile const int*)&st->flag) return;
+  for (int i = tid; i < kHotSampleHash; i += kThreads) { skey[i] = -1; scnt[i] = 0; }
+  for (int i = tid; i < kHotHash; i += kThreads) hkey[i] = -1;
+  if (tid == 0) nhot = 0;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSPer; ++j) {
+    const int row = samp[j];
+    if (row < 0 || (int64_t)row >= rows) continue;
+    unsigned h = ((unsigned)row * 2654435761u) & (kHotSampleHash - 1);
+    while (true) {
+      const int prev = atomicCAS(&skey[h], -1, row);
+      if (prev == -1 || prev == row) break;
+      h = (h + 1) & (kHotSampleHash - 1);
+    }
+    atomicAdd(&scnt[h], 1);
+  }
+  __syncthreads();
+  const int hmax = ha + hb;
+  for (int lo : {256, 64, 16, 4, 3}) {
+    for (int s = tid; s < kHotSampleHash; s += kThreads) {
+      const int c = scnt[s];
+      if (skey[s] != -1 && c >= lo) {
+        scnt[s] = 0;   // taken (or dropped) at this level
+        const int a = atomicAdd(&nhot, 1);
+        if (a < hmax) {
+          hrow[a] = skey[s];
+          unsigned h = ((unsigned)skey[s] * 2654435761u) & (kHotHash - 1);
+          while (atomicCAS(&hkey[h], -1, skey[s]) != -1) h = (h + 1) & (kHotHash - 1);
+          hslot[h] = a;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const int nh = nhot < hmax ? nhot : hmax;
+  const int na = nh < ha ? nh : ha, nb = nh - na;
+  // tier A is laid out [NW][na][q] (dense for the rows actually taken)
+  accB = accA + (size_t)NW * na * cols;
+  for (int t = tid; t < (NW * na + nb) * q; t += kThreads)
+    reinterpret_cast<float4*>(accA)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
   const float4* Y4 = reinterpret_cast<const float4*>(Y);
-  for (int64_t base = (int64_t)blockIdx.x * kAtTile; base < n; base += (int64_t)gridDim.x * kAtTile) {
-    const int cnt = (int)(n - base < kAtTile ? n - base : kAtTile);
-    for (int i = tid; i < kAtHash; i += kAtThreads) { hk[i] = -1; hc[i] = 0; }
-    if (tid == 0) nacc = 0;
-    __syncthreads();
-    for (int i = tid; i < cnt; i += kAtThreads) {
-      const int row = __ldg(I + base + i);
-      sI[i] = row;
-      unsigned h = ((unsigned)row * 2654435761u) & (kAtHash - 1);
-      while (true) {
-        const int prev = atomicCAS(&hk[h], -1, row);
-        if (prev == -1 || prev == row) break;
-        h = (h + 1) & (kAtHash - 1);
-      }
-      atomicAdd(&hc[h], 1);
-      eslot[i] = (short)h;
+  float4* accw = reinterpret_cast<float4*>(accA) + (size_t)warp * na * q;
+  const bool act = sub < per && gl < q;
+  float4 v[U];
+  int row[U];
+  auto load = [&](int64_t e0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * per + sub;
+      const bool ok = act && e < hi;
+      row[u] = ok ? __ldg(I + e) : -1;
+      v[u] = ok ? __ldcs(Y4 + (size_t)e * q + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    __syncthreads();
-    // accumulators go to the most repeated rows first (count >= 16, >= 4, >= 2);
-    // hc[s] becomes -(accumulator index) - 2 for a chosen row, a count otherwise
-    for (int lo : {16, 4, 2}) {
-      for (int s = tid; s < kAtHash; s += kAtThreads) {
-        const int c = hc[s];
-        if (hk[s] != -1 && c >= lo) {
-          const int a = atomicAdd(&nacc, 1);
-          if (a < amax) { arow[a] = hk[s]; hc[s] = -a - 2; }
+  };
+  int64_t e0 = lo + (int64_t)warp * per * U;
+  load(e0);   // in flight across the grid barrier
+  grid_barrier(&st->hot_arrivals);
+  if (blockIdx.x == 0 && tid == 0) { st->hot[par ^ 1].flag = 0; st->hot[par ^ 1].nbad = 0ull; }
+  if (*(volatile const int*)&st->hot[par].flag) return;
+  for (; e0 < hi; e0 += (int64_t)NW * per * U) {
+    if (e0 != lo + (int64_t)warp * per * U) load(e0);
+    int slots[U];
+    if (nh > 0) {   // first probes of all U rows issued together; collisions walk on
+      unsigned hh[U];
+      int kk[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        hh[u] = ((unsigned)row[u] * 2654435761u) & (kHotHash - 1);
+        kk[u] = row[u] >= 0 ? hkey[hh[u]] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        while (kk[u] != -1 && kk[u] != row[u]) {
+          hh[u] = (hh[u] + 1) & (kHotHash - 1);
+          kk[u] = hkey[hh[u]];
         }
+        slots[u] = kk[u] == row[u] && row[u] >= 0 ? hslot[hh[u]] : -1;
       }
-      __syncthreads();
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) slots[u] = -1;
     }
-    for (int s = tid; s < kAtHash; s += kAtThreads) hc[s] = hc[s] <= -2 ? -hc[s] - 2 : -1;
-    __syncthreads();
-    const int na = nacc < amax ? nacc : amax;
-    for (int t = tid; t < na * q; t += kAtThreads) reinterpret_cast<float4*>(acc)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncthreads();
-    // stream the tile's Y rows once: lane group `sub` takes entries e, e + per, ...
-    // (4 in flight per lane), one float4 per lane (q <= 32 quads per row)
-    constexpr int U = 4;
-    for (int e0 = warp * per * U; e0 < cnt; e0 += NWp * per * U) {
-      float4 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * per + sub;
-        v[u] = (sub < per && e < cnt && gl < q) ? __ldcs(Y4 + (size_t)(base + e) * q + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = 0; u < U; ++u) {
+      const int slot = slots[u];
+      if (row[u] >= 0 && slot < 0) red_add_v4(W + (size_t)row[u] * cols + 4 * gl, v[u]);
+      if (slot >= na) {
+        float* p = accB + (size_t)(slot - na) * cols + 4 * gl;
+        atomicAdd(p, v[u].x); atomicAdd(p + 1, v[u].y); atomicAdd(p + 2, v[u].z); atomicAdd(p + 3, v[u].w);
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * per + sub;
-        if (sub < per && e < cnt && gl < q) {
-          const int a = hc[eslot[e]];
-          if (a < 0) {
-            red_add_v4(W + (size_t)sI[e] * cols + 4 * gl, v[u]);
-          } else {
-            float* d = acc + (size_t)a * cols + 4 * gl;
-            atomicAdd(d, v[u].x); atomicAdd(d + 1, v[u].y); atomicAdd(d + 2, v[u].z); atomicAdd(d + 3, v[u].w);
+      const bool isA = slot >= 0 && slot < na;
+      if (__any_sync(0xffffffffu, isA)) {
+        for (int hs = 0; hs < per; ++hs) {
+          if (sub == hs && isA) {
+            float4* p = accw + slot * q + gl;
+            float4 t = *p;
+            t.x += v[u].x; t.y += v[u].y; t.z += v[u].z; t.w += v[u].w;
+            *p = t;
           }
+          __syncwarp();
         }
       }
     }
-    __syncthreads();
-    for (int t = tid; t < na * q; t += kAtThreads) {
-      const int a = t / q, f = t - a * q;
-      red_add_v4(W + (size_t)arow[a] * cols + 4 * f, reinterpret_cast<const float4*>(acc)[t]);
+  }
+  __syncthreads();
+  for (int t = tid; t < nh * q; t += kThreads) {
+    const int r = t / q, f = t - r * q;
+    float4 s;
+    if (r < na) {
+      const float4* a = reinterpret_cast<const float4*>(accA) + (size_t)r * q + f;
+      s = a[0];
+      for (int w = 1; w < NW; ++w) {
+        const float4 b = a[(size_t)w * na * q];
+        s.x += b.x; s.y += b.y; s.z += b.z; s.w += b.w;
+      }
+    } else {
+      s = reinterpret_cast<const float4*>(accB)[(size_t)(r - na) * q + f];
     }
-    __syncthreads();
+    red_add_v4(W + (size_t)hrow[r] * cols + 4 * f, s);
   }
 }
 
@@ -763,26 +876,27 @@ __global__ void sc_atomic_scalar(const int32_t* __restrict__ I, const float* __r
 }
 
 // ------------------------------------------------------------------ host side
-// sc_atomic_coop configuration: (threads, tile entries, hash slots, smem budget).
-// Measured on the 1M-row microbench (Zipf / uniform): 512 x 2048 at 2 CTAs/SM
-// 120 / 93 us; 256 x 1024 at 4/SM 115 / 99 us; 1024 x 8192 at 1/SM 124 / 101 us.
-struct AtCfg {
-  int threads, tile, hash;
-  size_t budget;
-  const void* fn;
-};
-static const AtCfg kAtCfgs[] = {
-    {512, 2048, 4096, 110 * 1024, (const void*)sc_atomic_coop<512, 2048, 4096>},
-};
-static const int g_at_cfg = 0;
-static bool g_sort_coop_ok = false;   // sc_sort_coop fits 1 CTA/SM (scatter_prepare)
-static int g_at_blocks_per_sm = 0;   // sc_atomic_coop occupancy (scatter_prepare)
-static size_t at_fixed(const AtCfg& c) { return sizeof(int) * (2 * c.hash + c.tile) + sizeof(short) * c.tile; }
-static int at_amax(const AtCfg& c, int cols) {   // accumulator rows that fit
-  const int a = (int)((c.budget - at_fixed(c)) / (sizeof(float) * cols));
-  return a < 160 ? a : 160;
+
+// sc_atomic_hot: 1024 threads (32 warps: enough rows in flight to stream Y),
+// 4 rows in flight per lane group; 512-thread variants measured 20-30 % slower.
+constexpr int kHotThreads = 1024;
+constexpr size_t kHotSmemMax = 200 * 1024;
+static const void* const kHotFn = (const void*)sc_atomic_hot<kHotThreads, 4>;
+// tier-A rows per warp and tier-B rows for a row width: tier A gets up to 32
+// rows if the warps' copies fit in half the budget, tier B the rest (<= kHotB).
+static void hot_tiers(int cols, int* ha, int* hb) {
+  const size_t row = sizeof(float) * cols, nw = kHotThreads / 32;
+  int a = (int)((kHotSmemMax * 2 / 3) / (nw * row));
+  *ha = a > 32 ? 32 : a;
+  int b = (int)((kHotSmemMax - (size_t)*ha * nw * row) / row);
+  *hb = b > kHotB ? kHotB : b;
 }
-static size_t at_smem(const AtCfg& c, int cols) { return at_fixed(c) + sizeof(float) * at_amax(c, cols) * cols; }
+static size_t hot_smem(int ha, int hb, int cols) {
+  const size_t acc = sizeof(float) * ((size_t)(kHotThreads / 32) * ha + hb) * cols;
+  const size_t samp = sizeof(int) * 2 * kHotSampleHash;
+  return acc > samp ? acc : samp;
+}
+static bool g_sort_coop_ok = false;   // sc_sort_coop fits 1 CTA/SM (scatter_prepare)
 static int bits_for(int64_t rows) {
   int b = 1;
   while (b < 31 && ((int64_t)1 << b) < rows) ++b;
@@ -836,27 +950,28 @@ static size_t downsweep_smem(int bins) {
 
 cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t rows, int cols,
                            const float* Y, const int32_t* I, int64_t n, int mode, cudaStream_t s,
-                           int* launches) {
+                           int* launches, unsigned long long epoch, int* slot) {
   unsigned char* b = static_cast<unsigned char*>(ws);
   ScatterStatus* st = reinterpret_cast<ScatterStatus*>(b + pl.off_status);
-  cudaError_t e = cudaMemsetAsync(b, 0, pl.zero_bytes, s);
+  *slot = -1;
+  cudaError_t e;
+  if (mode == 1 && (cols & 3) == 0 && cols <= 128) {
+    int ha, hb;
+    hot_tiers(cols, &ha, &hb);
+    const size_t smem = hot_smem(ha, hb, cols);
+    int par = (int)(epoch & 1);
+    void* args[] = {(void*)&I, (void*)&Y, (void*)&W, (void*)&rows, (void*)&cols, (void*)&n,
+                    (void*)&ha, (void*)&hb, (void*)&st, (void*)&par};
+    *launches += 1;
+    *slot = par;
+    return cudaLaunchCooperativeKernel(kHotFn, pl.num_sms, kHotThreads, args, smem, s);
+  }
+  e = cudaMemsetAsync(b, 0, pl.zero_bytes, s);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(&st->bad, 0xff, sizeof(st->bad), s);   // "no bad index"
   if (e != cudaSuccess) return e;
   const int blocks = pl.num_sms * 4;
   if (mode == 1) {
-    if ((cols & 3) == 0 && cols <= 128 && g_at_blocks_per_sm > 0) {
-      const AtCfg& c = kAtCfgs[g_at_cfg];
-      const size_t smem = at_smem(c, cols);
-      int bps = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, c.fn, c.threads, smem) != cudaSuccess || bps < 1)
-        bps = g_at_blocks_per_sm;
-      int grid = bps * pl.num_sms;
-      int amax = at_amax(c, cols);
-      void* args[] = {(void*)&I, (void*)&Y, (void*)&W, (void*)&rows, (void*)&cols, (void*)&n, (void*)&amax, (void*)&st};
-      *launches += 1;
-      return cudaLaunchCooperativeKernel(c.fn, grid, c.threads, args, smem, s);
-    }
     sc_validate<<<blocks, 256, 0, s>>>(I, n, rows, st);
     if ((cols & 3) == 0) sc_atomic<<<blocks * 2, 256, 0, s>>>(I, Y, W, cols, n, st);
     else sc_atomic_scalar<<<blocks * 2, 256, 0, s>>>(I, Y, W, cols, n, st);
@@ -935,11 +1050,8 @@ cudaError_t scatter_prepare(int bins) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sc_upsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(int) * (kSortThreads / 32) * bins));
-  for (const AtCfg& c : kAtCfgs)
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.budget);
-  if (e == cudaSuccess)   // co-resident CTAs per SM at the largest row width (cols = 128)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_at_blocks_per_sm, kAtCfgs[g_at_cfg].fn,
-                                                      kAtCfgs[g_at_cfg].threads, at_smem(kAtCfgs[g_at_cfg], 128));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kHotFn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHotSmemMax);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sc_reduce<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reduce_smem(4));
   if (e == cudaSuccess)

@@ -10,7 +10,13 @@ struct ScatterStatus {
   int flag;                 // 1: an index was out of range -> nothing applied
   int pad;
   unsigned long long bad;   // min over (position << 32 | uint32 value)
-  unsigned long long arrivals;   // grid-barrier counter of the cooperative atomic kernel
+  unsigned long long arrivals;   // grid-barrier counter of the cooperative kernels
+  // sc_atomic_hot (no per-call memset): call e uses hot[e & 1] and clears
+  // hot[(e + 1) & 1] for the next call; nbad = ~(position << 32 | value),
+  // max-reduced, so 0 means "no bad index".  hot_arrivals is its own
+  // monotonic barrier counter (fixed grid size).
+  struct { int flag; int pad; unsigned long long nbad; } hot[2];
+  unsigned long long hot_arrivals;
 };
 
 struct ScatterPlan {
@@ -23,8 +29,10 @@ struct ScatterPlan {
 ScatterPlan scatter_plan(int64_t rows, int cols, int64_t n, int num_sms);
 int scatter_supported(int cols, int mode);
 cudaError_t scatter_prepare(int bins);
+// epoch: per-workspace call counter; *slot = -1 if the call reports through
+// (flag, bad), else the hot[] slot it used.
 cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t rows, int cols,
                            const float* Y, const int32_t* I, int64_t n, int mode, cudaStream_t s,
-                           int* launches);
+                           int* launches, unsigned long long epoch, int* slot);
 
 }  // namespace pg

@@ -1,0 +1,1 @@
+python scripts/scatter_bench.py atomic

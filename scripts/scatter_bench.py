@@ -28,6 +28,8 @@ for dist_name in ("zipf", "uniform"):
         tms = []
         for _ in range(10):
             flush.zero_()
+            if os.environ.get("SLEEP"):
+                torch.cuda._sleep(int(os.environ["SLEEP"]))
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             pg.pg_scatter_add_async(W, Yd, Id, mode=mode)
@@ -35,4 +37,13 @@ for dist_name in ("zipf", "uniform"):
             tms.append((a, b))
         torch.cuda.synchronize()
         us = statistics.median([a.elapsed_time(b) for a, b in tms]) * 1e3
-        print(f"{dist_name:8s} {mode_name:6s} {us:7.1f} us  {alg / us / 1e3:6.0f} GB/s  max|err| vs fp64 {err:.2e}")
+        # back to back (no flush in between; Y is 10x larger than L2 anyway)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(20):
+            pg.pg_scatter_add_async(W, Yd, Id, mode=mode)
+        b.record()
+        torch.cuda.synchronize()
+        bb = a.elapsed_time(b) * 1e3 / 20
+        print(f"{dist_name:8s} {mode_name:6s} {us:7.1f} us  {alg / us / 1e3:6.0f} GB/s  (back-to-back {bb:6.1f} us)"
+              f"  max|err| vs fp64 {err:.2e}")

@@ -122,3 +122,65 @@ def test_empty_is_noop(env):
     W = torch.ones(10, 64, device="cuda")
     pg.pg_scatter_add(W, torch.zeros(0, 64, device="cuda"), torch.zeros(0, dtype=torch.int32, device="cuda"))
     assert bool((W == 1).all())
+
+
+def test_atomic_error_slots_alternate(env):
+    """ATOMIC reports through two status slots used on alternate calls (no
+    per-call reset): a bad call, then good calls, then a bad one must each
+    report their own outcome, and only the good ones change W."""
+    pg, torch = env
+    rows, cols, n = 500, 64, 3000
+    I, Y = synth.scatter_inputs(rows, cols, n, "zipf", "int", seed=5)
+    Yd = torch.from_numpy(Y).cuda()
+    bad = I.copy()
+    bad[17] = -3
+    W = torch.zeros(rows, cols, device="cuda")
+    ref = np.zeros((rows, cols), np.float64)
+    for k, ok in enumerate([False, True, True, False, False, True]):
+        Id = torch.from_numpy(I if ok else bad).cuda()
+        if ok:
+            pg.pg_scatter_add(W, Yd, Id, mode=pg.PG_SCATTER_ATOMIC)
+            ref = oracle.index_add(ref, Y.astype(np.float64), I)
+        else:
+            with pytest.raises(pg.PGError) as e:
+                pg.pg_scatter_add(W, Yd, Id, mode=pg.PG_SCATTER_ATOMIC)
+            assert e.value.status == pg.PG_ERANGE and "position 17" in str(e.value), k
+        assert np.array_equal(W.cpu().numpy(), ref.astype(np.float32)), k
+
+
+def test_atomic_async_err_flag(env):
+    pg, torch = env
+    rows, cols, n = 200, 16, 1000
+    I, Y = synth.scatter_inputs(rows, cols, n, "uniform", "int", seed=6)
+    I[999] = rows
+    W = torch.zeros(rows, cols, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for k in range(3):   # both status slots
+        pg.pg_scatter_add_async(W, torch.from_numpy(Y).cuda(), torch.from_numpy(I).cuda(),
+                                mode=pg.PG_SCATTER_ATOMIC, err_flag=flag)
+        torch.cuda.synchronize()
+        assert int(flag.item()) == 1 and bool((W == 0).all()), k
+        flag.zero_()
+
+
+def test_unaligned_rejected(env):
+    pg, torch = env
+    buf = torch.zeros(10 * 64 + 1, device="cuda")
+    W = buf[1:].view(10, 64)   # 4-byte aligned only
+    with pytest.raises(pg.PGError) as e:
+        pg.pg_scatter_add(W, torch.ones(3, 64, device="cuda"), torch.zeros(3, dtype=torch.int32, device="cuda"),
+                          mode=pg.PG_SCATTER_ATOMIC)
+    assert e.value.status == pg.PG_EINVAL
+
+
+@pytest.mark.parametrize("cols", [4, 12, 64, 128])
+def test_atomic_hot_rows_int_payload_bitwise(env, cols):
+    """Heavily repeated rows (every tier of the ATOMIC hot set: a 30 % row,
+    a Zipf head, single-use rows) with integer payloads: every summation order
+    is exact, so ATOMIC must equal the serial oracle bitwise at every width."""
+    rng = np.random.default_rng(cols)
+    rows, n = 5000, 200_000
+    I = np.where(rng.random(n) < 0.3, 7, rng.zipf(1.3, n) % rows).astype(np.int32)
+    Y = rng.integers(-8, 9, (n, cols)).astype(np.float32)
+    ref = oracle.index_add(np.zeros((rows, cols), np.float32), Y, I)
+    assert np.array_equal(gpu_scatter(env, np.zeros((rows, cols), np.float32), Y, I, 1), ref)
