@@ -7,7 +7,8 @@
  * centre c = floor(n/2) and corrupt centre word corr[k]:
  *   x   = concat_p C[idx[k][p]]                 gather  (dual of PAPER.md:98-102)
  *   x'  = x with block c replaced by C[corr[k]]
- *   a   = W1^T x + b1,  z = hardtanh(a) = clamp(a, -1, 1)       (north_star)
+ *   a   = W1^T x + b1,  z = hardtanh(a) = clamp(a, -1, 1)       (north_star;
+ *                        tanh instead with PG_OPT_ACTIVATION = PG_ACT_TANH)
  *   s   = w2 . z + b2;  s' likewise for x'
  *   l_k = max(0, 1 - s + s')                    (north_star)
  *   L   = (1/B) sum_k l_k                       (mean, reading G4)
@@ -80,11 +81,20 @@ enum {
   PG_OPT_RESERVE = 4, /* value: batch size; allocates the step workspace for it now
                          (so later steps at <= that batch never allocate -- e.g.
                          before CUDA-graph capture).  PG_EINVAL unless 1..2^30. */
-  PG_OPT_TRACE = 5    /* value: (int64_t) device pointer to >= 64*P uint64 slots, 0 = off.
+  PG_OPT_TRACE = 5,   /* value: (int64_t) device pointer to >= 64*P uint64 slots, 0 = off.
                          Per-CTA %globaltimer stamps of the step's stages; honoured
                          only by the instrumented build libpg_trace.so (-DPG_TRACE),
                          ignored by libpg.so.  For scripts/trace_step.py. */
+  PG_OPT_ACTIVATION = 6 /* value: PG_ACT_HARDTANH (default) or PG_ACT_TANH; applies
+                           to pg_train_step* and pg_score from the next call on.
+                           PG_EINVAL for any other value. */
 };
+
+/* Hidden-layer nonlinearity f (PG_OPT_ACTIVATION).  HARDTANH: f(a) =
+ * clamp(a, -1, 1), f'(a) = 1 for |a| < 1 and 0 otherwise (north_star; SENNA's
+ * HardTanh; subgradient 0 at |a| = 1).  TANH: f(a) = tanh(a), f'(a) =
+ * 1 - tanh(a)^2 (the CPU spec's model). */
+enum { PG_ACT_HARDTANH = 0, PG_ACT_TANH = 1 };
 
 /* pg_init -- allocate a model on the current CUDA device and initialise it:
  * C ~ U[-0.5, 0.5), W1 ~ U[-0.5/(window*dim), +), w2 ~ U[-0.5/hidden, +),
@@ -112,7 +122,7 @@ pg_status pg_train_step(pg_model* m, const int32_t* idx_batch,
 float pg_train_step_loss(pg_model* m, const int32_t* idx_batch,
                          const int32_t* corrupt_idx, int32_t batch, float lr);
 
-/* pg_score -- s = w2 . hardtanh(W1^T x + b1) + b2 for each window
+/* pg_score -- s = w2 . f(W1^T x + b1) + b2 for each window (f: PG_OPT_ACTIVATION)
  * (SPEC.md:204-212).  Blocking if scores_out is host memory, else asynchronous. */
 pg_status pg_score(pg_model* m, const int32_t* idx_batch, int32_t batch,
                    float* scores_out);

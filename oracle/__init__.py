@@ -17,6 +17,8 @@ Parity pins for every function (none is "parity unpinned"):
     10000-ones example (SPEC.md:130), decomposability (SPEC.md:81-84);
   * pgo_train_step(_dp)      -- zero-params fixed point, b2 invariance,
     locality (SPEC.md:244), DP emulation == single step up to rounding;
+  * tanh variant (pgo_set_activation(1)) -- finite differences (smooth, no
+    kinks), the h=1 closed form s = tanh(c), zero-params fixed point;
   * pgo_init_params          -- golden hash under tests/golden/ written by a
     script that calls only this package, plus range/moment checks.
 See tests/test_oracle_*.py.
@@ -50,6 +52,30 @@ def build(force: bool = False) -> str:
     return _SO
 
 
+HARDTANH, TANH = 0, 1
+
+
+class activation:
+    """Context manager: the oracle's nonlinearity inside the block
+    (HARDTANH: north_star / reading G1; TANH: SPEC.md:70, 205), restored after."""
+
+    _cur = HARDTANH
+
+    def __init__(self, act):
+        self.act = act
+
+    def __enter__(self):
+        self.prev = activation._cur
+        if lib().pgo_set_activation(self.act) != 0:
+            raise ValueError(f"unknown activation {self.act}")
+        activation._cur = self.act
+        return self
+
+    def __exit__(self, *exc):
+        lib().pgo_set_activation(self.prev)
+        activation._cur = self.prev
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -70,6 +96,8 @@ def lib():
         L.pgo_index_add.argtypes = [P, i64, i32, P, P, i64]
         L.pgo_index_add_f32.argtypes = [P, i64, i32, P, P, i64]
         L.pgo_last_bad.argtypes = [P, P]
+        L.pgo_set_activation.argtypes = [i32]
+        L.pgo_set_activation.restype = ctypes.c_int
         for f in ("pgo_init_params", "pgo_forward", "pgo_backward", "pgo_score",
                   "pgo_train_step", "pgo_train_step_dp", "pgo_index_add",
                   "pgo_index_add_f32"):

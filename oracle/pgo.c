@@ -96,6 +96,22 @@ int pgo_init_params(int64_t V, int d, int n, int h, uint64_t seed,
 /* ---------------------------------------------------------------------- */
 static double hardtanh(double a) { return a < -1.0 ? -1.0 : (a > 1.0 ? 1.0 : a); }
 
+/* Nonlinearity switch: 0 = hardtanh (north_star,
+ * G1), 1 = tanh.  Process-wide; test infrastructure. */
+static int g_act = 0;
+int pgo_set_activation(int act) {
+  if (act != 0 && act != 1) return PGO_EINVAL;
+  g_act = act;
+  return PGO_OK;
+}
+static double act_f(double a) { return g_act ? tanh(a) : hardtanh(a); }
+/* f'(a): hardtanh' = 1 strictly inside (-1, 1), 0 at and beyond +-1 (G2);
+ * tanh' = 1 - tanh(a)^2. */
+static double act_d(double a) {
+  if (g_act) { const double t = tanh(a); return 1.0 - t * t; }
+  return fabs(a) < 1.0 ? 1.0 : 0.0;
+}
+
 static void build_window(int d, int n, const double* C, const int32_t* tokens,
                          double* x) {
   for (int p = 0; p < n; ++p)
@@ -110,7 +126,7 @@ static double score_window(int d, int n, int h, const double* W1,
     double acc = b1[u];
     for (int i = 0; i < n * d; ++i) acc += x[i] * W1[(int64_t)i * h + u];
     a[u] = acc;
-    s += w2[u] * hardtanh(acc);
+    s += w2[u] * act_f(acc);
   }
   return s;
 }
@@ -174,8 +190,8 @@ int pgo_score(int64_t V, int d, int n, int h, const double* C, const double* W1,
 /* inv_batch * sum_k max(0, m_k) w.r.t. every parameter, all at the        */
 /* pre-step parameters.  For each k with m > 0 (G3: subgradient 0 at 0):   */
 /*   g = -inv_batch (d m/d s = -1), g' = +inv_batch (d m/d s' = +1)         */
-/*   delta  = g  * w2 .* [|a|  < 1]     (G2: hardtanh' = 0 at |a| = 1)     */
-/*   delta' = g' * w2 .* [|a'| < 1]                                         */
+/*   delta  = g  * w2 .* f'(a)   (hardtanh: [|a| < 1], G2; tanh: 1 - z^2)  */
+/*   delta' = g' * w2 .* f'(a')                                             */
 /*   dW1 += x delta^T + x' delta'^T;  db1 += delta + delta';                */
 /*   dw2 += g z + g' z';  db2 += g + g'                                     */
 /*   dx = W1 delta, dx' = W1 delta'  -> 2n rows (idx[k][p], dx_p) then      */
@@ -215,15 +231,15 @@ int pgo_backward(int64_t V, int d, int n, int h, const double* C,
     if (!(m > 0.0)) continue;                      /* inactive hinge */
     double g = -inv_batch, gc = +inv_batch;
     for (int u = 0; u < h; ++u) {
-      delta[u] = fabs(a[u]) < 1.0 ? g * w2[u] : 0.0;
-      deltac[u] = fabs(ac[u]) < 1.0 ? gc * w2[u] : 0.0;
+      delta[u] = g * w2[u] * act_d(a[u]);
+      deltac[u] = gc * w2[u] * act_d(ac[u]);
     }
     for (int i = 0; i < nd; ++i)
       for (int u = 0; u < h; ++u)
         dW1[(int64_t)i * h + u] += x[i] * delta[u] + xc[i] * deltac[u];
     for (int u = 0; u < h; ++u) {
       db1[u] += delta[u] + deltac[u];
-      dw2[u] += g * hardtanh(a[u]) + gc * hardtanh(ac[u]);
+      dw2[u] += g * act_f(a[u]) + gc * act_f(ac[u]);
     }
     *db2 += g + gc;
     /* dx = W1 delta (true window), then dx' = W1 delta' (corrupt window) */

@@ -13,6 +13,7 @@
  *   x_k   = concat_p C[idx[k][p]]                       (gather dual)
  *   x'_k  = x_k with block c=floor(n/2) := C[corr[k]]
  *   a     = W1^T x + b1,  z = hardtanh(a) = clamp(a,-1,1) (BASELINE.json north_star)
+ *           or z = tanh(a) after pgo_set_activation(1)
  *   s     = w2 . z + b2,  m = 1 - s + s',  l = max(0, m)
  *   L     = (1/B) sum_k l_k                              (reading G4)
  *   backward by hand, subgradient 0 at |a|=1 and at m=0  (readings G2, G3)
@@ -76,6 +77,8 @@ int pgo_index_add_f32(float* W, int64_t rows, int cols, const float* Y,
                       const int32_t* I, int64_t n);
 
 void pgo_last_bad(int64_t* position, int64_t* value);
+/* 0 = hardtanh (default), 1 = tanh; process-wide. */
+int pgo_set_activation(int act);
 
 #ifdef __cplusplus
 }

@@ -57,6 +57,7 @@ struct pg_model {
   DevStatus* st_host = nullptr;  // pinned mirror for blocking reads
   cudaStream_t stream = nullptr;
   int mode = PG_SCATTER_DET, fused = 1, fast = 0;
+  int act = PG_ACT_HARDTANH;
   size_t smem_max = 0;
   unsigned long long* trace = nullptr;
   // per-batch workspace (capacity grows)
@@ -118,11 +119,11 @@ __global__ void transpose_w1_kernel(const float* __restrict__ W1, float* __restr
   }
 }
 
-// Warp per window: s = w2 . clamp(W1^T x + b1, -1, 1) + b2.
+// Warp per window: s = w2 . f(W1^T x + b1) + b2, f = hardtanh or tanh.
 __global__ void score_kernel(const float* __restrict__ C, const float* __restrict__ W1,
                              const float* __restrict__ b1, const float* __restrict__ w2,
                              const float* __restrict__ b2, int64_t V, int d, int n, int h,
-                             const int32_t* __restrict__ idx, int B, float* out, DevStatus* st) {
+                             const int32_t* __restrict__ idx, int B, float* out, DevStatus* st, int act) {
   extern __shared__ float xsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nd = n * d;
@@ -145,7 +146,7 @@ __global__ void score_kernel(const float* __restrict__ C, const float* __restric
     for (int u = lane; u < h; u += 32) {
       float a = __ldg(b1 + u);
       for (int i = 0; i < nd; ++i) a = fmaf(x[i], __ldg(W1 + (size_t)i * h + u), a);
-      sp += __ldg(w2 + u) * fminf(fmaxf(a, -1.f), 1.f);
+      sp += __ldg(w2 + u) * act_f(a, act);
     }
     const float s = warp_sum(sp) + __ldg(b2);
     bad = __any_sync(0xffffffffu, bad);
@@ -381,6 +382,11 @@ extern "C" pg_status pg_set_option(pg_model* m, int key, int64_t value) {
     case PG_OPT_FUSED:
       m->fused = value ? 1 : 0;
       return PG_OK;
+    case PG_OPT_ACTIVATION:
+      if (value != PG_ACT_HARDTANH && value != PG_ACT_TANH)
+        return fail(PG_EINVAL, "PG_OPT_ACTIVATION: unknown nonlinearity %lld", (long long)value);
+      m->act = (int)value;
+      return PG_OK;
     case PG_OPT_TRACE:   // device buffer of [P][32] u64 stage stamps (libpg_trace.so), 0 = off
       m->trace = reinterpret_cast<unsigned long long*>(value);
       return PG_OK;
@@ -535,7 +541,7 @@ extern "C" pg_status pg_score(pg_model* m, const int32_t* idx_batch, int32_t bat
   int blocks = (batch + warps - 1) / warps;
   if (blocks > m->num_sms * 16) blocks = m->num_sms * 16;
   score_kernel<<<blocks, warps * 32, sm, m->stream>>>(m->C, m->W1, m->b1, m->w2, m->b2, m->V, m->d, m->n, m->h,
-                                                      di, batch, out, m->st);
+                                                      di, batch, out, m->st, m->act);
   m->launches += 1;
   CU(cudaGetLastError());
   if (pg_status s = consume_inputs(m)) return s;
@@ -569,6 +575,7 @@ static StepParams make_params(pg_model* m, const Geometry& g, const int32_t* idx
   p.V = m->V; p.d = m->d; p.n = m->n; p.h = m->h;
   p.idx = idx; p.corr = corr; p.B = B;
   p.inv_B = 1.0f / (float)((int64_t)B * m->world);
+  p.act = m->act;
   p.lr = lr;
   p.P = g.P; p.R = g.R; p.T = g.T; p.cap = g.cap;
   p.dense_part = m->dense_part;

@@ -37,6 +37,26 @@ __device__ __forceinline__ float4 ldcg4(const float* p) {
   return __ldcg(reinterpret_cast<const float4*>(p));
 }
 
+// ---------------------------------------------------------------- nonlinearity
+// act 0: hardtanh z = clamp(a, -1, 1) (north_star; reading G1), derivative 1
+// strictly inside (-1, 1), 0 at and beyond |a| = 1 (G2); act 1: z = tanh(a),
+// derivative 1 - z^2.
+__device__ __forceinline__ float act_f(float a, int act) {
+  return act ? tanhf(a) : fminf(fmaxf(a, -1.f), 1.f);
+}
+// gw * f'(a) given z = f(a); the hardtanh branch is a select (no multiply), so
+// that path's bits are unchanged by the switch.
+__device__ __forceinline__ float act_g(float gw, float a, float z, int act) {
+  return act ? gw * (1.f - z * z) : (fabsf(a) < 1.f ? gw : 0.f);
+}
+// sigma = delta + delta' for the context rows, delta = gw f'(a), delta' =
+// -gw f'(a').  For tanh, (1 - z^2) - (1 - z'^2) cancels in fp32 (z^2 is small
+// next to 1, so the difference keeps ~1e-4 relative accuracy); the same value
+// is formed as gw (z' - z)(z' + z).  Hardtanh keeps delta + delta'.
+__device__ __forceinline__ float act_sigma(float gw, float z, float zc, float dl, float dlc, int act) {
+  return act ? gw * ((zc - z) * (zc + z)) : dl + dlc;
+}
+
 // ---------------------------------------------------------------- grid barrier
 // Barrier for a cooperative (co-resident) grid on a monotonic 64-bit arrival
 // counter that is never reset: every instance adds exactly gridDim.x, so the

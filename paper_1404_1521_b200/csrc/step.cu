@@ -560,8 +560,8 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
         const float base = b1 + actx[k];
         a[k] = base + acen[k];
         ac[k] = base + acor[k];
-        z[k] = fminf(fmaxf(a[k], -1.f), 1.f);
-        zc[k] = fminf(fmaxf(ac[k], -1.f), 1.f);
+        z[k] = act_f(a[k], p.act);
+        zc[k] = act_f(ac[k], p.act);
         sp[k] = w2 * z[k];
         spc[k] = w2 * zc[k];
       }
@@ -582,12 +582,13 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
         const float m = 1.f - sv + svc;
         const bool active = m > 0.f;
         const float g = active ? -p.inv_B : 0.f;
-        const float dl = fabsf(a[k]) < 1.f ? g * w2 : 0.f;
-        const float dlc = fabsf(ac[k]) < 1.f ? -g * w2 : 0.f;
-        sig[(0 * T + ee) * 32 + lane] = dl + dlc;
+        const float dl = act_g(g * w2, a[k], z[k], p.act);
+        const float dlc = act_g(-g * w2, ac[k], zc[k], p.act);
+        const float sg = act_sigma(g * w2, z[k], zc[k], dl, dlc, p.act);
+        sig[(0 * T + ee) * 32 + lane] = sg;
         sig[(1 * T + ee) * 32 + lane] = dl;
         sig[(2 * T + ee) * 32 + lane] = dlc;
-        acc_db1 += dl + dlc;
+        acc_db1 += sg;
         acc_dw2 += g * z[k] + (-g) * zc[k];
         if (lane == 0) acc_hinge += active ? m : 0.f;
       }
@@ -724,8 +725,8 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
           a[k] = ctx + part[((size_t)c * kTT + e) * h + u];
           ac[k] = ctx + part[((size_t)n * kTT + e) * h + u];
           w2v[k] = __ldg(p.w2 + u);
-          sp += w2v[k] * fminf(fmaxf(a[k], -1.f), 1.f);
-          spc += w2v[k] * fminf(fmaxf(ac[k], -1.f), 1.f);
+          sp += w2v[k] * act_f(a[k], p.act);
+          spc += w2v[k] * act_f(ac[k], p.act);
         }
       }
       sp = warp_sum(sp);
@@ -737,13 +738,14 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
       for (int k = 0; k < 4; ++k) {
         const int u = lane + 32 * k;
         if (u < h) {
-          const float dl = fabsf(a[k]) < 1.f ? g * w2v[k] : 0.f;
-          const float dlc = fabsf(ac[k]) < 1.f ? -g * w2v[k] : 0.f;
-          const float z = fminf(fmaxf(a[k], -1.f), 1.f), zc = fminf(fmaxf(ac[k], -1.f), 1.f);
-          SU[((size_t)0 * h + u) * kXTS + e] = dl + dlc;
+          const float z = act_f(a[k], p.act), zc = act_f(ac[k], p.act);
+          const float dl = act_g(g * w2v[k], a[k], z, p.act);
+          const float dlc = act_g(-g * w2v[k], ac[k], zc, p.act);
+          const float sg = act_sigma(g * w2v[k], z, zc, dl, dlc, p.act);
+          SU[((size_t)0 * h + u) * kXTS + e] = sg;
           SU[((size_t)1 * h + u) * kXTS + e] = dl;
           SU[((size_t)2 * h + u) * kXTS + e] = dlc;
-          SE[((size_t)0 * kTT + e) * h + u] = dl + dlc;
+          SE[((size_t)0 * kTT + e) * h + u] = sg;
           SE[((size_t)1 * kTT + e) * h + u] = dl;
           SE[((size_t)2 * kTT + e) * h + u] = dlc;
           DW[(size_t)e * h + u] = g * z + (-g) * zc;
@@ -958,8 +960,8 @@ __device__ void phase1_generic(const StepParams& p, unsigned char* sm) {
       float sp = 0.f, spc = 0.f;
       for (int u = lane; u < h; u += 32) {
         const float w2 = __ldg(p.w2 + u);
-        sp += w2 * fminf(fmaxf(A[e * h + u], -1.f), 1.f);
-        spc += w2 * fminf(fmaxf(Ac[e * h + u], -1.f), 1.f);
+        sp += w2 * act_f(A[e * h + u], p.act);
+        spc += w2 * act_f(Ac[e * h + u], p.act);
       }
       const float s = warp_sum(sp) + b2, sc = warp_sum(spc) + b2;
       const float m = 1.f - s + sc;
@@ -967,9 +969,10 @@ __device__ void phase1_generic(const StepParams& p, unsigned char* sm) {
       const float g = active ? -p.inv_B : 0.f;
       for (int u = lane; u < h; u += 32) {
         const float w2 = __ldg(p.w2 + u);
-        const float dl = fabsf(A[e * h + u]) < 1.f ? g * w2 : 0.f;
-        const float dlc = fabsf(Ac[e * h + u]) < 1.f ? -g * w2 : 0.f;
-        DEL[e * h + u] = dl; DELc[e * h + u] = dlc; SIG[e * h + u] = dl + dlc;
+        const float dl = act_g(g * w2, A[e * h + u], act_f(A[e * h + u], p.act), p.act);
+        const float dlc = act_g(-g * w2, Ac[e * h + u], act_f(Ac[e * h + u], p.act), p.act);
+        DEL[e * h + u] = dl; DELc[e * h + u] = dlc;
+        SIG[e * h + u] = act_sigma(g * w2, act_f(A[e * h + u], p.act), act_f(Ac[e * h + u], p.act), dl, dlc, p.act);
       }
       if (lane == 0) { gz[e] = g; hinge_s[e] = active ? m : 0.f; }
     }
@@ -989,8 +992,8 @@ __device__ void phase1_generic(const StepParams& p, unsigned char* sm) {
       float db = 0.f, dw = 0.f;
       for (int e = 0; e < cnt; ++e) {
         db += SIG[e * h + u];
-        const float z = fminf(fmaxf(A[e * h + u], -1.f), 1.f);
-        const float zc = fminf(fmaxf(Ac[e * h + u], -1.f), 1.f);
+        const float z = act_f(A[e * h + u], p.act);
+        const float zc = act_f(Ac[e * h + u], p.act);
         dw += gz[e] * z + (-gz[e]) * zc;
       }
       rec[ndh + u] = first ? db : rec[ndh + u] + db;

@@ -167,6 +167,7 @@ struct StepParams {
   const int32_t* corr;
   int B;
   float inv_B;   // 1 / global batch
+  int act;       // 0 hardtanh, 1 tanh (PG_OPT_ACTIVATION)
   float lr;
   // decomposition
   int P, R, T, cap;     // cap = (n+1)*T list capacity

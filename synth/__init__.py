@@ -13,7 +13,10 @@ workload (SURVEY.md §8(d) "Synthetic inputs"):
   * scatter microbench: I ~ Zipf or uniform over the table rows, Y ~ U[-1, 1)
     float32 or integer-valued in [-8, 8] (the exact-sum mode, SPEC.md:130);
   * random parameter sets for parity cases (the library's pg_set_params and
-    the oracle receive the same float32 values).
+    the oracle receive the same float32 values);
+  * a bigram-structured corpus for the convergence study (SURVEY.md §8(f)
+    NEXT-1): a first-order Markov chain in which every word has `branching`
+    successors, the next token uniform among them.
 
 Every draw is a pure function of (seed, stream id, step, element index).
 """
@@ -29,6 +32,7 @@ _M2 = np.uint64(0x94D049BB133111EB)
 
 # stream ids (any distinct constants)
 S_TOKENS, S_CORRUPT, S_IID, S_SCATTER_I, S_SCATTER_Y, S_PARAMS = 11, 12, 13, 21, 22, 31
+S_BIGRAM_SUCC, S_BIGRAM_WALK, S_BIGRAM_POS = 41, 42, 43
 
 
 def _mix(z: np.ndarray) -> np.ndarray:
@@ -156,3 +160,27 @@ def random_params(V: int, d: int, n: int, h: int, seed: int, c_scale: float = 0.
     b1 = (u[o:o + h] * b1_scale).astype(np.float32); o += h
     w2 = (u[o:o + h] * w2_scale).astype(np.float32)
     return C, W1, b1, w2, np.float32(b2)
+
+
+def bigram_corpus(V: int, length: int, seed: int = 42, branching: int = 4) -> np.ndarray:
+    """Token stream [length] int32 of a first-order Markov chain over [0, V):
+    word w's successors are succ[w][0..branching-1] (uniform draws), the next
+    token is one of them, uniformly.  Consecutive windows therefore carry a
+    learnable structure that a uniformly corrupted centre breaks."""
+    succ = uniform_ids(V, V * branching, seed, S_BIGRAM_SUCC, 0).reshape(V, branching)
+    pick = (bits(seed, S_BIGRAM_WALK, 0, 0, length) % np.uint64(branching)).astype(np.int64)
+    toks = np.empty(length, np.int32)
+    w = int(uniform_ids(V, 1, seed, S_BIGRAM_WALK, 1)[0])
+    for i in range(length):
+        toks[i] = w
+        w = int(succ[w, pick[i]])
+    return toks
+
+
+def corpus_batch(toks: np.ndarray, V: int, n: int, B: int, seed: int, step: int, lo: int = 0, hi: int = -1):
+    """B windows at i.i.d. uniform start positions in toks[lo:hi] and their
+    corrupt centres (uniform, != centre)."""
+    hi = toks.shape[0] if hi < 0 else hi
+    starts = lo + (bits(seed, S_BIGRAM_POS, step, 0, B) % np.uint64(hi - lo - n + 1)).astype(np.int64)
+    idx = np.ascontiguousarray(toks[starts[:, None] + np.arange(n)[None, :]], dtype=np.int32)
+    return idx, corrupt_centres(V, idx[:, n // 2], seed, step)

@@ -354,3 +354,60 @@ def test_dp_emulation_equals_single_step():
     lb = oracle.train_step_dp(b, idx, corr, 0.1, world=4)
     assert abs(la - lb) <= 1e-14
     np.testing.assert_allclose(b.flat(), a.flat(), rtol=1e-13, atol=1e-16)
+
+
+# ---------------------------------------------------------------- tanh variant
+def test_tanh_score_closed_form():
+    # SPEC.md:211 with the spec's own nonlinearity: h=1, W1=0,
+    # b1=[c], w2=[1], b2=0 -> s = tanh(c) for every window
+    V, d, n = 7, 3, 5
+    idx, _ = synth.batch(V, n, 4, seed=5, kind="uniform")
+    with oracle.activation(oracle.TANH):
+        for c in (-3.0, -1.0, -0.25, 0.0, 0.5, 1.0, 2.0):
+            p = oracle.Params(V, d, n, 1, C=np.ones((V, d)), b1=[c], w2=[1.0])
+            np.testing.assert_allclose(oracle.score(p, idx), np.tanh(c), rtol=0, atol=1e-15)
+    p = oracle.Params(V, d, n, 1, C=np.ones((V, d)), b1=[3.0], w2=[1.0])
+    assert (oracle.score(p, idx) == 1.0).all()      # the switch is restored (hardtanh clamps)
+
+
+def test_tanh_zero_params_fixed_point():
+    V, d, n, h = 30, 4, 5, 8
+    p = oracle.Params(V, d, n, h)
+    idx, corr = synth.batch(V, n, 16, seed=3)
+    with oracle.activation(oracle.TANH):
+        for _ in range(2):
+            assert oracle.train_step(p, idx, corr, 0.1) == 1.0
+    assert not p.flat().any()
+
+
+def test_tanh_finite_differences():
+    # tanh is smooth: only the hinge kink m = 0 has to be avoided.  Large
+    # weights make some units saturate (tanh' ~ 0) and some margins negative.
+    good, seed = 0, 500
+    saw_sat = saw_inactive = False
+    with oracle.activation(oracle.TANH):
+        while good < 8:
+            seed += 1
+            p, idx, corr = _saturating_fixture(seed, w1x=120.0)
+            f = oracle.forward(p, idx, corr)
+            m = 1 - f["s"] + f["s_corr"]
+            if np.abs(m).min() < 1e-4:
+                continue
+            saw_sat |= bool((np.abs(f["a"]) > 2).any())
+            saw_inactive |= bool((m < 0).any())
+            g = _fd_check(p, idx, corr)
+            assert np.abs(g).max() > 0
+            good += 1
+    assert saw_sat and saw_inactive
+
+
+def test_tanh_differs_from_hardtanh_inside():
+    # the switch really changes the arithmetic (|a| < 1: tanh(a) != a)
+    V, d, n, h = 40, 4, 5, 6
+    p = oracle.Params.init(V, d, n, h, 3)
+    p.W1 *= 30
+    idx, corr = synth.batch(V, n, 8, seed=4)
+    l_hard = oracle.loss(p, idx, corr)
+    with oracle.activation(oracle.TANH):
+        l_tanh = oracle.loss(p, idx, corr)
+    assert abs(l_hard - l_tanh) > 1e-6
