@@ -85,10 +85,17 @@ enum {
                          Per-CTA %globaltimer stamps of the step's stages; honoured
                          only by the instrumented build libpg_trace.so (-DPG_TRACE),
                          ignored by libpg.so.  For scripts/trace_step.py. */
-  PG_OPT_ACTIVATION = 6 /* value: PG_ACT_HARDTANH (default) or PG_ACT_TANH; applies
-                           to pg_train_step* and pg_score from the next call on.
-                           PG_EINVAL for any other value. */
+  PG_OPT_ACTIVATION = 6, /* value: PG_ACT_HARDTANH (default) or PG_ACT_TANH; applies
+                            to pg_train_step* and pg_score from the next call on.
+                            PG_EINVAL for any other value. */
+  PG_OPT_REDUCTION = 7   /* value: PG_REDUCE_MEAN (default: L = (1/B) sum_k l_k and
+                            its gradient, B the global batch; reading G4) or
+                            PG_REDUCE_SUM (L = sum_k l_k: the same step as MEAN at
+                            lr * B; the reading PAPER.md:197-198 hints at).
+                            PG_EINVAL for any other value. */
 };
+
+enum { PG_REDUCE_MEAN = 0, PG_REDUCE_SUM = 1 };
 
 /* Hidden-layer nonlinearity f (PG_OPT_ACTIVATION).  HARDTANH: f(a) =
  * clamp(a, -1, 1), f'(a) = 1 for |a| < 1 and 0 otherwise (north_star; SENNA's

@@ -19,6 +19,9 @@ Parity pins for every function (none is "parity unpinned"):
     locality (SPEC.md:244), DP emulation == single step up to rounding;
   * tanh variant (pgo_set_activation(1)) -- finite differences (smooth, no
     kinks), the h=1 closed form s = tanh(c), zero-params fixed point;
+  * sum reduction (pgo_set_reduction(1)) -- exact identities with the mean
+    form (loss x B; one step at lr equals the mean step at lr x B for
+    power-of-two B) and finite differences of the summed loss;
   * pgo_init_params          -- golden hash under tests/golden/ written by a
     script that calls only this package, plus range/moment checks.
 See tests/test_oracle_*.py.
@@ -76,6 +79,30 @@ class activation:
         activation._cur = self.prev
 
 
+MEAN, SUM = 0, 1
+
+
+class reduction:
+    """Context manager: batch reduction of the loss and its gradient inside the
+    block (MEAN: reading G4; SUM: the summed-loss reading)."""
+
+    _cur = MEAN
+
+    def __init__(self, red):
+        self.red = red
+
+    def __enter__(self):
+        self.prev = reduction._cur
+        if lib().pgo_set_reduction(self.red) != 0:
+            raise ValueError(f"unknown reduction {self.red}")
+        reduction._cur = self.red
+        return self
+
+    def __exit__(self, *exc):
+        lib().pgo_set_reduction(self.prev)
+        reduction._cur = self.prev
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -98,6 +125,8 @@ def lib():
         L.pgo_last_bad.argtypes = [P, P]
         L.pgo_set_activation.argtypes = [i32]
         L.pgo_set_activation.restype = ctypes.c_int
+        L.pgo_set_reduction.argtypes = [i32]
+        L.pgo_set_reduction.restype = ctypes.c_int
         for f in ("pgo_init_params", "pgo_forward", "pgo_backward", "pgo_score",
                   "pgo_train_step", "pgo_train_step_dp", "pgo_index_add",
                   "pgo_index_add_f32"):
@@ -180,7 +209,7 @@ def loss(p: Params, idx, corr) -> float:
 def backward(p: Params, idx, corr, inv_batch=None):
     idx, corr = _i32(idx), _i32(corr)
     B = corr.shape[0]
-    inv = 1.0 / B if inv_batch is None else float(inv_batch)
+    inv = (1.0 if reduction._cur == SUM else 1.0 / B) if inv_batch is None else float(inv_batch)
     dW1 = np.zeros_like(p.W1); db1 = np.zeros(p.h); dw2 = np.zeros(p.h); db2 = np.zeros(1)
     rows = np.zeros(2 * p.n * B, dtype=np.int32)
     Y = np.zeros((2 * p.n * B, p.d))

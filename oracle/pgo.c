@@ -104,6 +104,17 @@ int pgo_set_activation(int act) {
   g_act = act;
   return PGO_OK;
 }
+/* Batch reduction (reading G4 / SURVEY.md §8(f) NEXT-2): 0 = mean (default:
+ * L = (1/B) sum l_k, gradients likewise), 1 = sum (L = sum l_k, the reading
+ * PAPER.md:197-198 hints at).  Process-wide; test infrastructure. */
+static int g_sum = 0;
+int pgo_set_reduction(int sum) {
+  if (sum != 0 && sum != 1) return PGO_EINVAL;
+  g_sum = sum;
+  return PGO_OK;
+}
+static double batch_scale(int64_t B) { return g_sum ? 1.0 : 1.0 / (double)B; }
+
 static double act_f(double a) { return g_act ? tanh(a) : hardtanh(a); }
 /* f'(a): hardtanh' = 1 strictly inside (-1, 1), 0 at and beyond +-1 (G2);
  * tanh' = 1 - tanh(a)^2. */
@@ -164,7 +175,7 @@ int pgo_forward(int64_t V, int d, int n, int h, const double* C,
     double m = 1.0 - s + sc;                       /* SPEC.md:216 */
     hinge_sum += m > 0.0 ? m : 0.0;
   }
-  if (loss_out) *loss_out = hinge_sum / (double)B;  /* mean, reading G4 */
+  if (loss_out) *loss_out = hinge_sum * batch_scale(B);  /* mean (reading G4) or sum */
   free(x); free(a); free(tk);
   return PGO_OK;
 }
@@ -342,7 +353,7 @@ int pgo_train_step(int64_t V, int d, int n, int h, double* C, double* W1,
   double* Y = malloc(sizeof(double) * 2 * n * B * d);
   int64_t nrows = 0;
   rc = pgo_backward(V, d, n, h, C, W1, b1, w2, b2, idx, corr, B,
-                    1.0 / (double)B, dW1, db1, dw2, &db2, rows, Y, &nrows);
+                    batch_scale(B), dW1, db1, dw2, &db2, rows, Y, &nrows);
   if (!rc)
     rc = apply_update(V, d, n, h, C, W1, b1, w2, b2, lr, dW1, db1, dw2, db2,
                       rows, Y, nrows);
@@ -372,7 +383,7 @@ int pgo_train_step_dp(int64_t V, int d, int n, int h, double* C, double* W1,
     double lg;
     pgo_forward(V, d, n, h, C, W1, b1, w2, b2, idx + g * Bl * n, corr + g * Bl,
                 Bl, NULL, NULL, NULL, NULL, &lg);
-    loss += lg * (double)Bl / (double)B;
+    loss += g_sum ? lg : lg * (double)Bl / (double)B;
   }
   if (loss_out) *loss_out = loss;
   if (!isfinite(loss)) return PGO_EDIVERGED;
@@ -390,7 +401,7 @@ int pgo_train_step_dp(int64_t V, int d, int n, int h, double* C, double* W1,
   for (int g = 0; g < world; ++g) {
     int64_t nr = 0;
     pgo_backward(V, d, n, h, C, W1, b1, w2, b2, idx + g * Bl * n, corr + g * Bl,
-                 Bl, 1.0 / (double)B, gW1, gb1, gw2, &gb2, rows + nrows,
+                 Bl, batch_scale(B), gW1, gb1, gw2, &gb2, rows + nrows,
                  Y + nrows * d, &nr);
     nrows += nr;
     for (int64_t i = 0; i < nd * h; ++i) dW1[i] += gW1[i];

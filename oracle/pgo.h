@@ -79,6 +79,8 @@ int pgo_index_add_f32(float* W, int64_t rows, int cols, const float* Y,
 void pgo_last_bad(int64_t* position, int64_t* value);
 /* 0 = hardtanh (default), 1 = tanh; process-wide. */
 int pgo_set_activation(int act);
+/* 0 = mean over the batch (default, reading G4), 1 = sum; process-wide. */
+int pgo_set_reduction(int sum);
 
 #ifdef __cplusplus
 }

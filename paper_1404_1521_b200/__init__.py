@@ -26,7 +26,9 @@ LIB_PATH = os.path.join(_HERE, "libpg_trace.so" if os.environ.get("PG_LIB_VARIAN
 PG_OK, PG_EINVAL, PG_ERANGE, PG_ENOMEM, PG_ECUDA, PG_ENCCL, PG_EDIVERGED = range(7)
 PG_SCATTER_DET, PG_SCATTER_ATOMIC = 0, 1
 PG_OPT_SCATTER, PG_OPT_STREAM, PG_OPT_FUSED, PG_OPT_RESERVE, PG_OPT_TRACE, PG_OPT_ACTIVATION = 1, 2, 3, 4, 5, 6
+PG_OPT_REDUCTION = 7
 PG_ACT_HARDTANH, PG_ACT_TANH = 0, 1
+PG_REDUCE_MEAN, PG_REDUCE_SUM = 0, 1
 
 EXPORTED = [
     "pg_init", "pg_train_step", "pg_train_step_loss", "pg_score", "pg_free", "pg_last_error",
@@ -244,7 +246,7 @@ class PolyglotModel:
     """Owns a pg_model handle; methods forward to the C ABI with the torch stream."""
 
     def __init__(self, vocab, dim, window, hidden, seed=42, scatter=PG_SCATTER_DET, stream=None,
-                 fused=True, activation=PG_ACT_HARDTANH):
+                 fused=True, activation=PG_ACT_HARDTANH, reduction=PG_REDUCE_MEAN):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("PolyglotModel needs a CUDA device (no CPU fallback)")
@@ -254,6 +256,7 @@ class PolyglotModel:
         pg_set_option(self.handle, PG_OPT_SCATTER, scatter)
         pg_set_option(self.handle, PG_OPT_FUSED, 1 if fused else 0)
         pg_set_option(self.handle, PG_OPT_ACTIVATION, activation)
+        pg_set_option(self.handle, PG_OPT_REDUCTION, reduction)
 
     def set_stream(self, stream):
         pg_set_option(self.handle, PG_OPT_STREAM, _stream_handle(stream))

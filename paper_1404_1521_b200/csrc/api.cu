@@ -58,6 +58,7 @@ struct pg_model {
   cudaStream_t stream = nullptr;
   int mode = PG_SCATTER_DET, fused = 1, fast = 0;
   int act = PG_ACT_HARDTANH;
+  int reduce_sum = 0;   // PG_OPT_REDUCTION
   size_t smem_max = 0;
   unsigned long long* trace = nullptr;
   // per-batch workspace (capacity grows)
@@ -387,6 +388,11 @@ extern "C" pg_status pg_set_option(pg_model* m, int key, int64_t value) {
         return fail(PG_EINVAL, "PG_OPT_ACTIVATION: unknown nonlinearity %lld", (long long)value);
       m->act = (int)value;
       return PG_OK;
+    case PG_OPT_REDUCTION:
+      if (value != PG_REDUCE_MEAN && value != PG_REDUCE_SUM)
+        return fail(PG_EINVAL, "PG_OPT_REDUCTION: unknown reduction %lld", (long long)value);
+      m->reduce_sum = value == PG_REDUCE_SUM;
+      return PG_OK;
     case PG_OPT_TRACE:   // device buffer of [P][32] u64 stage stamps (libpg_trace.so), 0 = off
       m->trace = reinterpret_cast<unsigned long long*>(value);
       return PG_OK;
@@ -574,7 +580,7 @@ static StepParams make_params(pg_model* m, const Geometry& g, const int32_t* idx
   p.C = m->C; p.W1 = m->W1; p.W1T = m->W1T; p.b1 = m->b1; p.w2 = m->w2; p.b2 = m->b2;
   p.V = m->V; p.d = m->d; p.n = m->n; p.h = m->h;
   p.idx = idx; p.corr = corr; p.B = B;
-  p.inv_B = 1.0f / (float)((int64_t)B * m->world);
+  p.inv_B = m->reduce_sum ? 1.0f : 1.0f / (float)((int64_t)B * m->world);
   p.act = m->act;
   p.lr = lr;
   p.P = g.P; p.R = g.R; p.T = g.T; p.cap = g.cap;

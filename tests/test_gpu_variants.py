@@ -1,5 +1,5 @@
-"""GPU parity of the tanh nonlinearity variant (
-SPEC.md:70, 205; PG_OPT_ACTIVATION = PG_ACT_TANH) against the float64 oracle
+"""GPU parity of the model variants of SURVEY.md §8(f) NEXT-2: the tanh
+nonlinearity (PG_OPT_ACTIVATION = PG_ACT_TANH) and the summed-loss reduction (PG_OPT_REDUCTION) against the float64 oracle
 with its tanh switch, on all three phase-1 paths (generic: tiny config;
 register-blocked h = 32: Polyglot; tiled: h in [64, 128]), the scorer, the
 DP group step and DET reproducibility.  Tolerances: SURVEY.md §8(c) T1-T5."""
@@ -109,3 +109,33 @@ def test_tanh_group_step_matches_oracle_dp(pg, world):
     assert_parity(np.array(gl), np.array(rl), p0, outs[0], ref, tau_delta=2e-3)
     for mm in models:
         mm.close()
+
+
+# ---------------------------------------------------------------- sum reduction (PG_OPT_REDUCTION)
+@pytest.mark.parametrize("act", [0, 1], ids=["hardtanh", "tanh"])
+def test_sum_reduction_parity(pg, act):
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    B = 1024
+    m = pg.PolyglotModel(V, d, n, h, seed=42, activation=act, reduction=pg.PG_REDUCE_SUM)
+    with oracle.activation(act), oracle.reduction(oracle.SUM):
+        gl, rl, p0, pend, ref = run_both(m, V, d, n, h, B=B, steps=6, lr=0.1 / B)
+    assert gl[0] > 100        # a sum, not a mean
+    assert_parity(gl, rl, p0, pend, ref, tau_delta=2e-3)
+    m.close()
+
+
+def test_sum_equals_mean_at_scaled_lr(pg):
+    # one step of the summed loss at lr equals the mean step at lr * B; B and lr
+    # powers of two so the fp32 gradient scalings are exact and the DET results
+    # must agree bitwise (the loss differs by exactly B)
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    B = 2048
+    idx, corr = synth.batch(V, n, B, seed=6)
+    ms = pg.PolyglotModel(V, d, n, h, seed=8, reduction=pg.PG_REDUCE_SUM)
+    mm = pg.PolyglotModel(V, d, n, h, seed=8)
+    ls = ms.train_step(idx, corr, 2.0 ** -14)
+    lm = mm.train_step(idx, corr, 2.0 ** -14 * B)
+    assert ls == np.float32(lm) * B
+    for a, b in zip(ms.get_params(), mm.get_params()):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+    ms.close(); mm.close()

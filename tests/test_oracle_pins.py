@@ -411,3 +411,43 @@ def test_tanh_differs_from_hardtanh_inside():
     with oracle.activation(oracle.TANH):
         l_tanh = oracle.loss(p, idx, corr)
     assert abs(l_hard - l_tanh) > 1e-6
+
+
+# ---------------------------------------------------------------- sum reduction (reading G4 alternative)
+def test_sum_reduction_identities():
+    # sum_k l_k = B * mean, and (exact for B a power of two) one SGD step of the
+    # summed loss at lr is the mean step at lr * B
+    V, d, n, h, B = 60, 4, 5, 8, 16
+    p = oracle.Params.init(V, d, n, h, 9)
+    p.W1 *= 40
+    idx, corr = synth.batch(V, n, B, seed=2)
+    a, b = p.copy(), p.copy()
+    lm = oracle.train_step(a, idx, corr, 0.25 * B)
+    with oracle.reduction(oracle.SUM):
+        ls = oracle.train_step(b, idx, corr, 0.25)
+    assert ls == lm * B
+    np.testing.assert_array_equal(a.flat(), b.flat())
+    assert oracle.loss(p, idx, corr) == lm         # switch restored
+
+
+def test_sum_reduction_finite_differences():
+    with oracle.reduction(oracle.SUM):
+        for seed in (601, 602, 603):
+            p, idx, corr = _saturating_fixture(seed)
+            f = oracle.forward(p, idx, corr)
+            m = 1 - f["s"] + f["s_corr"]
+            if min(np.abs(m).min(), np.abs(np.abs(f["a"]) - 1).min(), np.abs(np.abs(f["a_corr"]) - 1).min()) < 1e-4:
+                continue
+            _fd_check(p, idx, corr)
+
+
+def test_sum_reduction_dp_emulation():
+    V, d, n, h = 300, 8, 5, 16
+    p = oracle.Params.init(V, d, n, h, 5)
+    idx, corr = synth.batch(V, n, 64, seed=8)
+    a, b = p.copy(), p.copy()
+    with oracle.reduction(oracle.SUM):
+        la = oracle.train_step(a, idx, corr, 0.01)
+        lb = oracle.train_step_dp(b, idx, corr, 0.01, world=4)
+    assert abs(la - lb) <= 1e-12 * abs(la)
+    np.testing.assert_allclose(b.flat(), a.flat(), rtol=1e-13, atol=1e-16)
