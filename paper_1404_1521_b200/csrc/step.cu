@@ -692,8 +692,13 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
       float2 acc[kTT];
 #pragma unroll
       for (int e = 0; e < kTT; ++e) acc[e] = make_float2(0.f, 0.f);
-#pragma unroll 8
-      for (int j = 0; j < d; ++j) {
+      // every CTA reads the same W1; rotating the start row per CTA spreads the
+      // simultaneous requests over the L2 slices instead of all CTAs hitting
+      // the same lines in lockstep
+      const int rot = (int)((blockIdx.x * 37u) % (unsigned)d);
+#pragma unroll 16
+      for (int jj = 0; jj < d; ++jj) {
+        const int j = jj + rot < d ? jj + rot : jj + rot - d;
         const float2 w = __ldg(wc + (size_t)j * H2);
 #pragma unroll
         for (int q = 0; q < kTT / 4; ++q) {
@@ -775,8 +780,10 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
         float2 acc[2][kTT / 2];
 #pragma unroll
         for (int q = 0; q < kTT / 2; ++q) acc[0][q] = acc[1][q] = make_float2(0.f, 0.f);
-#pragma unroll 4
-        for (int u = 0; u < h; ++u) {
+        const int rot = (int)((blockIdx.x * 37u) % (unsigned)h);   // as in the forward
+#pragma unroll 16
+        for (int uu = 0; uu < h; ++uu) {
+          const int u = uu + rot < h ? uu + rot : uu + rot - h;
           const float w0 = __ldg(wt + (size_t)u * nd), w1 = __ldg(wt + (size_t)u * nd + D2);
 #pragma unroll
           for (int q = 0; q < kTT / 4; ++q) {
