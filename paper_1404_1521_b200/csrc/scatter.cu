@@ -632,17 +632,20 @@ __global__ void sc_validate(const int32_t* __restrict__ I, int64_t n, int64_t ro
 // Zipf head row with 80k entries alone would take > 500 us
 // (scripts/micro/red_stream.cu, bulk_reduce.cu).  So:
 //  1. every CTA checks its grid-strided share of I (all loads issued at once)
-//     and, redundantly and identically, counts a fixed strided sample of
-//     kHotSample entries in an smem hash; rows seen >= 2 times in the sample
-//     (relative frequency >~ 0.05 %) become the CTA's hot set, most frequent
-//     first: the first ha go to tier A (a private accumulator per warp), the
-//     next up to kHotB to tier B (one shared accumulator per CTA);
-//  2. the CTA's first rows of Y are loaded, then the grid barrier (a bad index
-//     anywhere means nothing is applied);
-//  3. CTA b streams its contiguous share of entries once (Y read with
-//     evict-first loads, U rows in flight per lane group): a tier-A row is
-//     added into the warp's private accumulator (the warp's lane groups take
-//     turns, no atomics), a tier-B row with shared-memory atomics (rare
+//     and arrives at the grid barrier; while the barrier completes it
+//     prefetches its share of W into L2 (when W is small next to the L2) and,
+//     redundantly and identically, counts a fixed strided sample of
+//     kHotSample entries in an smem hash: rows seen >= 3 times (relative
+//     frequency >~ 0.07 %) become the CTA's hot set, rows seen >= 16 times
+//     first -- the first ha go to tier A (a private accumulator per warp),
+//     the next up to kHotB to tier B (one shared accumulator per CTA);
+//  2. barrier wait (a bad index anywhere means nothing is applied);
+//  3. warps take batches of 32 consecutive entries, interleaved over the
+//     grid: lane i loads I[b0 + i] and probes the hot set for it, then the
+//     lane groups stream the batch's Y rows (evict-first loads, U rows in
+//     flight per lane group; row and slot arrive by shuffles): a tier-A row
+//     is added into the warp's private accumulator (the warp's lane groups
+//     take turns, no atomics), a tier-B row with shared-memory atomics (rare
 //     collisions), every other row goes straight to W with
 //     red.global.add.v4.f32 per 16 B;
 //  4. the accumulators (tier A summed over warps in warp order) reach W with
@@ -679,15 +682,6 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     const int64_t i = (int64_t)j * kThreads + tid;
     samp[j] = i < ns ? __ldg(I + i * sstride) : -1;
   }
-  // W's first touch by a reduction after a cold L2 is an L2 miss the atomic
-  // unit waits on; when W is small next to the L2, pull it in while the
-  // prologue runs (this CTA's 1/gridDim share of its 128 B lines).
-  if ((size_t)rows * cols * sizeof(float) <= kHotPrefetchMax) {
-    const int64_t lines = ((int64_t)rows * cols * (int64_t)sizeof(float)) >> 7;
-    const char* wb = reinterpret_cast<const char*>(W);
-    for (int64_t l = (int64_t)blockIdx.x * kThreads + tid; l < lines; l += (int64_t)gridDim.x * kThreads)
-      asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(wb + (l << 7)));
-  }
   {   // validation: this CTA's grid-strided share, 4 x int4 per thread per trip
     const int64_t n4 = ((uintptr_t)I & 15) == 0 ? n >> 2 : 0;
     const int4* I4 = reinterpret_cast<const int4*>(I);
@@ -718,6 +712,17 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
       }
     }
   }
+  // Everything up to grid_wait is CTA-local: it overlaps the barrier.
+  const unsigned long long target = grid_arrive(&st->hot_arrivals);
+  // W's first touch by a reduction after a cold L2 is an L2 miss the atomic
+  // unit waits on; when W is small next to the L2, pull it in while the
+  // prologue runs (this CTA's 1/gridDim share of its 128 B lines).
+  if ((size_t)rows * cols * sizeof(float) <= kHotPrefetchMax) {
+    const int64_t lines = ((int64_t)rows * cols * (int64_t)sizeof(float)) >> 7;
+    const char* wb = reinterpret_cast<const char*>(W);
+    for (int64_t l = (int64_t)blockIdx.x * kThreads + tid; l < lines; l += (int64_t)gridDim.x * kThreads)
+      asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(wb + (l << 7)));
+  }
   for (int i = tid; i < kHotSampleHash; i += kThreads) { skey[i] = -1; scnt[i] = 0; }
   for (int i = tid; i < kHotHash; i += kThreads) hkey[i] = -1;
   if (tid == 0) nhot = 0;
@@ -736,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   }
   __syncthreads();
   const int hmax = ha + hb;
-  for (int lo : {256, 64, 16, 4, 3}) {
+  for (int lo : {16, 3}) {   // most frequent first: tier A gets rows seen >= 16 times
     for (int s = tid; s < kHotSampleHash; s += kThreads) {
       const int c = scnt[s];
       if (skey[s] != -1 && c >= lo) {
@@ -758,70 +763,68 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   accB = accA + (size_t)NW * na * cols;
   for (int t = tid; t < (NW * na + nb) * q; t += kThreads)
     reinterpret_cast<float4*>(accA)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
-  const float4* Y4 = reinterpret_cast<const float4*>(Y);
   float4* accw = reinterpret_cast<float4*>(accA) + (size_t)warp * na * q;
   const bool act = sub < per && gl < q;
-  float4 v[U];
-  int row[U];
-  auto load = [&](int64_t e0) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = e0 + u * per + sub;
-      const bool ok = act && e < hi;
-      row[u] = ok ? __ldg(I + e) : -1;
-      v[u] = ok ? __ldcs(Y4 + (size_t)e * q + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+  // Warp batches of 32 consecutive entries: lane i loads I[b0 + i] and probes
+  // the hot set once for it; the lane groups then take the batch's entries
+  // `per` at a time (U in flight), row and slot broadcast by shuffles.  Row and
+  // entry offsets are 32-bit (the host guarantees rows*cols, n*cols < 2^31).
+  auto probe = [&](int r) -> int {
+    unsigned hh = ((unsigned)r * 2654435761u) & (kHotHash - 1);
+    int k;
+    while ((k = hkey[hh]) != -1 && k != r) hh = (hh + 1) & (kHotHash - 1);
+    return k == r ? hslot[hh] : -1;
   };
-  int64_t e0 = lo + (int64_t)warp * per * U;
-  load(e0);   // in flight across the grid barrier
-  grid_barrier(&st->hot_arrivals);
+  // batches interleaved over the grid: at any moment the SMs stream
+  // neighbouring parts of Y
+  const int64_t gstride = (int64_t)gridDim.x * NW * 32;
+  int64_t b0 = ((int64_t)blockIdx.x * NW + warp) * 32;
+  const int64_t hi_all = n;
+  int rl = b0 + lane < hi_all ? __ldg(I + b0 + lane) : -1;   // in flight across the barrier wait
+  grid_wait(&st->hot_arrivals, target);
   if (blockIdx.x == 0 && tid == 0) { st->hot[par ^ 1].flag = 0; st->hot[par ^ 1].nbad = 0ull; }
   if (*(volatile const int*)&st->hot[par].flag) return;
-  for (; e0 < hi; e0 += (int64_t)NW * per * U) {
-    if (e0 != lo + (int64_t)warp * per * U) load(e0);
-    int slots[U];
-    if (nh > 0) {   // first probes of all U rows issued together; collisions walk on
-      unsigned hh[U];
-      int kk[U];
+  for (; b0 < hi_all; b0 += gstride) {
+    const int nb = hi_all - b0 < 32 ? (int)(hi_all - b0) : 32;
+    const int sl = (nh > 0 && rl >= 0) ? probe(rl) : -1;
+    const int64_t bn = b0 + gstride;
+    const int rn = bn + lane < hi_all ? __ldg(I + bn + lane) : -1;   // next batch's rows
+    const float4* Yb = reinterpret_cast<const float4*>(Y) + (size_t)b0 * q;
+    for (int k0 = 0; k0 < nb; k0 += per * U) {
+      float4 v[U];
+      int row[U], slot[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        hh[u] = ((unsigned)row[u] * 2654435761u) & (kHotHash - 1);
-        kk[u] = row[u] >= 0 ? hkey[hh[u]] : -1;
+        const int k = k0 + u * per + sub;
+        row[u] = __shfl_sync(0xffffffffu, rl, k & 31);
+        slot[u] = __shfl_sync(0xffffffffu, sl, k & 31);
+        const bool ok = act && k < nb;
+        if (!ok) row[u] = -1;
+        v[u] = ok ? __ldcs(Yb + k * q + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        while (kk[u] != -1 && kk[u] != row[u]) {
-          hh[u] = (hh[u] + 1) & (kHotHash - 1);
-          kk[u] = hkey[hh[u]];
+        const int sv = row[u] >= 0 ? slot[u] : -1;
+        if (row[u] >= 0 && sv < 0) red_add_v4(W + (row[u] * cols + 4 * gl), v[u]);
+        if (sv >= na) {
+          float* p = accB + (sv - na) * cols + 4 * gl;
+          atomicAdd(p, v[u].x); atomicAdd(p + 1, v[u].y); atomicAdd(p + 2, v[u].z); atomicAdd(p + 3, v[u].w);
         }
-        slots[u] = kk[u] == row[u] && row[u] >= 0 ? hslot[hh[u]] : -1;
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < U; ++u) slots[u] = -1;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int slot = slots[u];
-      if (row[u] >= 0 && slot < 0) red_add_v4(W + (size_t)row[u] * cols + 4 * gl, v[u]);
-      if (slot >= na) {
-        float* p = accB + (size_t)(slot - na) * cols + 4 * gl;
-        atomicAdd(p, v[u].x); atomicAdd(p + 1, v[u].y); atomicAdd(p + 2, v[u].z); atomicAdd(p + 3, v[u].w);
-      }
-      const bool isA = slot >= 0 && slot < na;
-      if (__any_sync(0xffffffffu, isA)) {
-        for (int hs = 0; hs < per; ++hs) {
-          if (sub == hs && isA) {
-            float4* p = accw + slot * q + gl;
-            float4 t = *p;
-            t.x += v[u].x; t.y += v[u].y; t.z += v[u].z; t.w += v[u].w;
-            *p = t;
+        const bool isA = sv >= 0 && sv < na;
+        if (__any_sync(0xffffffffu, isA)) {
+          for (int hs = 0; hs < per; ++hs) {
+            if (sub == hs && isA) {
+              float4* p = accw + sv * q + gl;
+              float4 t = *p;
+              t.x += v[u].x; t.y += v[u].y; t.z += v[u].z; t.w += v[u].w;
+              *p = t;
+            }
+            __syncwarp();
           }
-          __syncwarp();
         }
       }
     }
+    rl = rn;
   }
   __syncthreads();
   for (int t = tid; t < nh * q; t += kThreads) {
@@ -879,11 +882,14 @@ __global__ void sc_atomic_scalar(const int32_t* __restrict__ I, const float* __r
 
 // sc_atomic_hot: 1024 threads (32 warps: enough rows in flight to stream Y),
 // 4 rows in flight per lane group; 512-thread variants measured 20-30 % slower.
+// sc_atomic_hot launch shape: 1024 threads (32 warps, the most at 64 registers)
+// with 4 rows in flight per lane group; measured slower: 1024 x 2 / x 8 rows,
+// 768 x 8, 512 x 8 (scripts/ab_atomic.sh history in DESIGN.md 7.2).
 constexpr int kHotThreads = 1024;
-constexpr size_t kHotSmemMax = 200 * 1024;
 static const void* const kHotFn = (const void*)sc_atomic_hot<kHotThreads, 4>;
+constexpr size_t kHotSmemMax = 200 * 1024;
 // tier-A rows per warp and tier-B rows for a row width: tier A gets up to 32
-// rows if the warps' copies fit in half the budget, tier B the rest (<= kHotB).
+// rows if the warps' copies fit in 2/3 of the budget, tier B the rest (<= kHotB).
 static void hot_tiers(int cols, int* ha, int* hb) {
   const size_t row = sizeof(float) * cols, nw = kHotThreads / 32;
   int a = (int)((kHotSmemMax * 2 / 3) / (nw * row));
@@ -955,7 +961,7 @@ cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t ro
   ScatterStatus* st = reinterpret_cast<ScatterStatus*>(b + pl.off_status);
   *slot = -1;
   cudaError_t e;
-  if (mode == 1 && (cols & 3) == 0 && cols <= 128) {
+  if (mode == 1 && (cols & 3) == 0 && cols <= 128 && rows * cols < (1ll << 31) && n * cols < (1ll << 31)) {
     int ha, hb;
     hot_tiers(cols, &ha, &hb);
     const size_t smem = hot_smem(ha, hb, cols);
