@@ -1202,12 +1202,24 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
       #pragma unroll 1
       for (int sb0 = 0; sb0 < Mw; sb0 += lay.SB, par ^= 1) {
         const int sb1 = min(Mw, sb0 + lay.SB);
-        #pragma unroll 1
-        for (int t = tid; t < (sb1 - sb0) * d; t += NT) {
-          const int e = sb0 + t / d, f = t % d;
-          const unsigned long long k = keys[e];
-          const int L = (int)((k >> 8) & 0xffffff), rel = (int)(k & 0xff);
-          stage[t] = __ldcg(p.list_vals + list_index(p, L, loff[L] + rel) * d + f);
+        if ((d & 3) == 0) {   // 16 B pieces
+          const int Q = d >> 2;
+          #pragma unroll 4
+          for (int t = tid; t < (sb1 - sb0) * Q; t += NT) {
+            const int e = sb0 + t / Q, f = t - (t / Q) * Q;
+            const unsigned long long k = keys[e];
+            const int L = (int)((k >> 8) & 0xffffff), rel = (int)(k & 0xff);
+            reinterpret_cast<float4*>(stage)[t] =
+                __ldcg(reinterpret_cast<const float4*>(p.list_vals + list_index(p, L, loff[L] + rel) * d) + f);
+          }
+        } else {
+          #pragma unroll 1
+          for (int t = tid; t < (sb1 - sb0) * d; t += NT) {
+            const int e = sb0 + t / d, f = t % d;
+            const unsigned long long k = keys[e];
+            const int L = (int)((k >> 8) & 0xffffff), rel = (int)(k & 0xff);
+            stage[t] = __ldcg(p.list_vals + list_index(p, L, loff[L] + rel) * d + f);
+          }
         }
         __syncthreads();
         int slo = 0, shi = nseg_total - 1;
@@ -1215,22 +1227,77 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
           int mid = (slo + shi + 1) >> 1;
           if (seg[mid] <= sb0) slo = mid; else shi = mid - 1;
         }
-        #pragma unroll 1
-        for (int sidx = slo + warp; sidx < nseg_total && seg[sidx] < sb1; sidx += NW) {
-          const int s0 = seg[sidx], s1 = seg[sidx + 1];
-          const int a0 = max(s0, sb0), a1 = min(s1, sb1);
-          const bool cont = s0 < sb0, fin = s1 <= sb1;
-          const unsigned row = (unsigned)(keys[s0] >> 32);
+        if ((d & 3) == 0) {
+          // thread per (segment, float4): 4 fixed chains by the entry's offset
+          // from its segment start (so a long, hot segment is summed with 4-way
+          // ILP by d/4 threads instead of serially by one warp), combined as
+          // (c0 + c1) + (c2 + c3); a segment crossing the window end hands its
+          // 4 chains on through `carry` [2][4][d/4] float4.
+          int she = slo, hi2 = nseg_total;   // first segment starting at or after sb1
+          while (she < hi2) {
+            const int mid = (she + hi2) >> 1;
+            if (seg[mid] < sb1) she = mid + 1; else hi2 = mid;
+          }
+          const int Q = d >> 2, nsw = she - slo;
+          const float4* st4 = reinterpret_cast<const float4*>(stage);
+          float4* cr4 = reinterpret_cast<float4*>(carry);
           #pragma unroll 1
-          for (int f = lane; f < d; f += 32) {
-            float acc = cont ? carry[par * d + f] : 0.f;
-            #pragma unroll 1
-            for (int e = a0; e < a1; ++e) acc += stage[(e - sb0) * d + f];
+          for (int it = tid; it < nsw * Q; it += NT) {
+            const int sidx = slo + it / Q, qf = it - (it / Q) * Q;
+            const int s0 = seg[sidx], s1 = seg[sidx + 1];
+            const int a0 = max(s0, sb0), a1 = min(s1, sb1);
+            const bool cont = s0 < sb0, fin = s1 <= sb1;
+            float4 c[4];
+            #pragma unroll
+            for (int k = 0; k < 4; ++k)
+              c[k] = cont ? cr4[(par * 4 + k) * Q + qf] : make_float4(0.f, 0.f, 0.f, 0.f);
+            auto add = [&](int k, float4 v) {
+              #pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                if (kk == k) { c[kk].x += v.x; c[kk].y += v.y; c[kk].z += v.z; c[kk].w += v.w; }
+            };
+            int e = a0;
+            for (; e < a1 && ((e - s0) & 3); ++e) add((e - s0) & 3, st4[(e - sb0) * Q + qf]);
+            #pragma unroll 2
+            for (; e + 3 < a1; e += 4) {
+              const float4 v0 = st4[(e - sb0) * Q + qf], v1 = st4[(e + 1 - sb0) * Q + qf];
+              const float4 v2 = st4[(e + 2 - sb0) * Q + qf], v3 = st4[(e + 3 - sb0) * Q + qf];
+              add(0, v0); add(1, v1); add(2, v2); add(3, v3);
+            }
+            for (; e < a1; ++e) add((e - s0) & 3, st4[(e - sb0) * Q + qf]);
             if (fin) {
-              float* cp = p.C + (size_t)row * d + f;
-              *cp = __ldcg(cp) + nlr * acc;
+              const unsigned row = (unsigned)(keys[s0] >> 32);
+              float4 t;
+              t.x = (c[0].x + c[1].x) + (c[2].x + c[3].x);
+              t.y = (c[0].y + c[1].y) + (c[2].y + c[3].y);
+              t.z = (c[0].z + c[1].z) + (c[2].z + c[3].z);
+              t.w = (c[0].w + c[1].w) + (c[2].w + c[3].w);
+              float4* cp = reinterpret_cast<float4*>(p.C + (size_t)row * d) + qf;
+              const float4 o = __ldcg(cp);
+              *cp = make_float4(o.x + nlr * t.x, o.y + nlr * t.y, o.z + nlr * t.z, o.w + nlr * t.w);
             } else {
-              carry[(par ^ 1) * d + f] = acc;
+              #pragma unroll
+              for (int k = 0; k < 4; ++k) cr4[((par ^ 1) * 4 + k) * Q + qf] = c[k];
+            }
+          }
+        } else {
+          #pragma unroll 1
+          for (int sidx = slo + warp; sidx < nseg_total && seg[sidx] < sb1; sidx += NW) {
+            const int s0 = seg[sidx], s1 = seg[sidx + 1];
+            const int a0 = max(s0, sb0), a1 = min(s1, sb1);
+            const bool cont = s0 < sb0, fin = s1 <= sb1;
+            const unsigned row = (unsigned)(keys[s0] >> 32);
+            #pragma unroll 1
+            for (int f = lane; f < d; f += 32) {
+              float acc = cont ? carry[par * d + f] : 0.f;
+              #pragma unroll 1
+              for (int e = a0; e < a1; ++e) acc += stage[(e - sb0) * d + f];
+              if (fin) {
+                float* cp = p.C + (size_t)row * d + f;
+                *cp = __ldcg(cp) + nlr * acc;
+              } else {
+                carry[(par ^ 1) * d + f] = acc;
+              }
             }
           }
         }

@@ -144,7 +144,7 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   if (SB < 16) SB = 16;
   L.SB = SB;
   L.stagefb = o; o = align16(o + SB * d * 4);
-  L.carry = o; o = align16(o + 2 * d * 4);
+  L.carry = o; o = align16(o + 2 * 4 * d * 4);   // [2][4 chains][d]
   L.total2 = o > fast_end ? o : fast_end;
   return L;
 }
