@@ -1,1 +1,1 @@
-for c in 0; do python scripts/scatter_bench.py atomic; done
+python scripts/scatter_bench.py atomic
