@@ -150,11 +150,15 @@ def pg_set_option(handle, key, value):
     _check(lib().pg_set_option(handle, int(key), int(value)), "pg_set_option")
 
 
-def pg_train_step(handle, idx_batch, corrupt_idx, lr, loss_out="host"):
+_HOST = "host"
+
+
+def pg_train_step(handle, idx_batch, corrupt_idx, lr, loss_out=_HOST):
     """One SGD step.  loss_out="host" -> blocking, returns the float loss;
     a device float32 tensor -> asynchronous, loss written there; None -> async."""
     batch = int(corrupt_idx.shape[0])
-    if loss_out == "host":
+    # `is`, not `==`: comparing a torch tensor with a str costs ~13 us per call
+    if loss_out is _HOST or (isinstance(loss_out, str) and loss_out == "host"):
         out = ctypes.c_float()
         _check(lib().pg_train_step(handle, _ptr(idx_batch, np.int32), _ptr(corrupt_idx, np.int32),
                                    batch, float(lr), ctypes.cast(ctypes.byref(out), ctypes.c_void_p)),
