@@ -139,3 +139,36 @@ def test_sum_equals_mean_at_scaled_lr(pg):
     for a, b in zip(ms.get_params(), mm.get_params()):
         assert np.array_equal(np.asarray(a), np.asarray(b))
     ms.close(); mm.close()
+
+
+def test_tanh_atomic_scatter_parity(pg):
+    """tanh with the ATOMIC embedding update (per-row red.add: one fp32
+    rounding per occurrence, allowed for by c_roundings)."""
+    m = make(pg, POLY, seed=42, scatter=pg.PG_SCATTER_ATOMIC)
+    with oracle.activation(oracle.TANH):
+        gl, rl, p0, pend, ref = run_both(m, **POLY, B=1024, steps=6)
+    assert_parity(gl, rl, p0, pend, ref, tau_delta=2e-3, c_roundings=run_both.occurrences)
+    m.close()
+
+
+def test_train_step_loss_literal_form(pg):
+    """pg_train_step_loss (the north-star form returning the loss): equals the
+    oracle's loss; NaN plus a message naming the position on a bad index, and
+    no mutation."""
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    m = make(pg, POLY, seed=3)
+    idx, corr = synth.batch(V, n, 512, seed=9)
+    ref = oracle_from_gpu_params(m.get_params(), V, d, n, h)
+    with oracle.activation(oracle.TANH):
+        lr_ = oracle.loss(ref, idx, corr)
+    lg = pg.pg_train_step_loss(m.handle, idx, corr, 0.1)
+    assert abs(lg - lr_) <= 1e-4 * abs(lr_)
+    before = m.get_params()
+    bad = idx.copy()
+    bad[17, 3] = -1
+    assert np.isnan(pg.pg_train_step_loss(m.handle, bad, corr, 0.1))
+    msg = pg.pg_last_error()
+    assert f"flat position {17 * n + 3} (value -1)" in msg, msg
+    for a, b in zip(before, m.get_params()):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+    m.close()
