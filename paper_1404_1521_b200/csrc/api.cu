@@ -790,7 +790,7 @@ static pg_status scatter_common(float* W, int64_t rows, int32_t cols, const floa
     cudaFree(g_sc_ws[dev]);
     g_sc_ws[dev] = nullptr;
     CU(cudaMalloc(&g_sc_ws[dev], pl.total_bytes));
-    CU(cudaMemset(g_sc_ws[dev], 0, pl.zero_bytes));   // status block (sc_atomic_hot never clears it per call)
+    CU(cudaMemset(g_sc_ws[dev], 0, pl.total_bytes));   // status block and ATOMIC replica rows start zeroed
     g_sc_cap[dev] = pl.total_bytes;
     CU(scatter_prepare(1024));   // the largest digit table any plan uses
   }

@@ -635,41 +635,47 @@ __global__ void sc_validate(const int32_t* __restrict__ I, int64_t n, int64_t ro
 //     and arrives at the grid barrier; while the barrier completes it
 //     prefetches its share of W into L2 (when W is small next to the L2) and,
 //     redundantly and identically, counts a fixed strided sample of
-//     kHotSample entries in an smem hash: rows seen >= 3 times (relative
-//     frequency >~ 0.07 %) become the CTA's hot set, rows seen >= 16 times
-//     first -- the first ha go to tier A (a private accumulator per warp),
-//     the next up to kHotB to tier B (one shared accumulator per CTA);
+//     kHotSample entries in an smem hash: rows seen >= kHotMin times
+//     (relative frequency >~ 0.1 %) are ranked by (count desc, row asc) with a
+//     bitonic sort, so every CTA derives the same ranking -- the first ha go to
+//     tier A (a private smem accumulator per warp), the next up to kHotB to
+//     tier B (kHotRep replica rows each, in global memory);
 //  2. barrier wait (a bad index anywhere means nothing is applied);
 //  3. warps take batches of 32 consecutive entries, interleaved over the
 //     grid: lane i loads I[b0 + i] and probes the hot set for it, then the
 //     lane groups stream the batch's Y rows (evict-first loads, U rows in
 //     flight per lane group; row and slot arrive by shuffles): a tier-A row
 //     is added into the warp's private accumulator (the warp's lane groups
-//     take turns, no atomics), a tier-B row with shared-memory atomics (rare
-//     collisions), every other row goes straight to W with
-//     red.global.add.v4.f32 per 16 B;
-//  4. the accumulators (tier A summed over warps in warp order) reach W with
-//     one vector reduction per 16 B per CTA.
+//     take turns, no atomics), a tier-B row goes by red.global.add.v4.f32 to
+//     one of its replica rows (by entry position: 1/kHotRep of the per-line
+//     serialisation), every other row straight to W the same way;
+//  4. tier A (summed over warps in warp order) reaches W with one vector
+//     reduction per 16 B per CTA; after a second grid barrier, CTA c folds the
+//     replica rows of tier-B rows c, c + grid, ... into W and zeroes them for
+//     the next call.
 // Uniform indices thus stay one streaming pass, and a Zipf head row costs one
 // reduction per CTA instead of one per entry.
 constexpr int kHotSample = 4096;
 constexpr int kHotSampleHash = 8192;
 constexpr int kHotHash = 1024;
 constexpr int kHotB = 256;
+constexpr int kHotMin = 4;                          // sample count of a hot row
+constexpr int kHotCand = kHotSample / kHotMin;      // 1024: every row seen >= kHotMin times
+constexpr int kHotRep = 8;                          // replica rows per tier-B row
 constexpr size_t kHotPrefetchMax = 48u << 20;
 template <int kThreads, int U>
 __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __restrict__ I,
                                                              const float* __restrict__ Y, float* W, int64_t rows,
                                                              int cols, int64_t n, int ha, int hb,
-                                                             ScatterStatus* st, int par) {
+                                                             ScatterStatus* st, int par, float* rep) {
   constexpr int NW = kThreads / 32;
   extern __shared__ __align__(16) unsigned char ah_sm[];
   float* accA = reinterpret_cast<float*>(ah_sm);                                // [NW][ha][cols]
-  float* accB = accA + (size_t)NW * ha * cols;                                 // [hb][cols]
   int* skey = reinterpret_cast<int*>(ah_sm);   // [kHotSampleHash] (aliases the accumulators)
   int* scnt = skey + kHotSampleHash;           // [kHotSampleHash]
+  unsigned long long* cand = reinterpret_cast<unsigned long long*>(scnt + kHotSampleHash);   // [kHotCand]
   __shared__ int hkey[kHotHash], hslot[kHotHash], hrow[32 + kHotB];
-  __shared__ int nhot;
+  __shared__ int ncand;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q = cols >> 2;
   const int G = q >= 32 ? 32 : q, per = 32 / G, sub = lane / G, gl = lane % G;
@@ -725,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   }
   for (int i = tid; i < kHotSampleHash; i += kThreads) { skey[i] = -1; scnt[i] = 0; }
   for (int i = tid; i < kHotHash; i += kThreads) hkey[i] = -1;
-  if (tid == 0) nhot = 0;
+  if (tid == 0) ncand = 0;
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kSPer; ++j) {
@@ -740,28 +746,43 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     atomicAdd(&scnt[h], 1);
   }
   __syncthreads();
-  const int hmax = ha + hb;
-  for (int lo : {16, 3}) {   // most frequent first: tier A gets rows seen >= 16 times
-    for (int s = tid; s < kHotSampleHash; s += kThreads) {
-      const int c = scnt[s];
-      if (skey[s] != -1 && c >= lo) {
-        scnt[s] = 0;   // taken (or dropped) at this level
-        const int a = atomicAdd(&nhot, 1);
-        if (a < hmax) {
-          hrow[a] = skey[s];
-          unsigned h = ((unsigned)skey[s] * 2654435761u) & (kHotHash - 1);
-          while (atomicCAS(&hkey[h], -1, skey[s]) != -1) h = (h + 1) & (kHotHash - 1);
-          hslot[h] = a;
-        }
-      }
+  // candidates: rows seen >= kHotMin times (<= kHotSample / kHotMin = kHotCand
+  // of them), ranked by (count desc, row asc) with a bitonic sort, so every
+  // CTA derives the same ranking -- tier B's replica rows in global memory
+  // must mean the same row in every CTA
+  for (int s2 = tid; s2 < kHotSampleHash; s2 += kThreads)
+    if (skey[s2] != -1 && scnt[s2] >= kHotMin) {
+      const int a = atomicAdd(&ncand, 1);
+      cand[a] = ((unsigned long long)(kHotSample - scnt[s2]) << 32) | (unsigned)skey[s2];
     }
-    __syncthreads();
+  __syncthreads();
+  const int nc = ncand;
+  int npow = 1;
+  while (npow < nc) npow <<= 1;
+  for (int i = nc + tid; i < npow; i += kThreads) cand[i] = ~0ull;
+  __syncthreads();
+  for (int size = 2; size <= npow; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = tid; t < npow / 2; t += kThreads) {
+        const int lo2 = 2 * t - (t & (stride - 1)), hi2 = lo2 + stride;
+        const bool up = (lo2 & size) == 0;
+        const unsigned long long x = cand[lo2], y = cand[hi2];
+        if ((x > y) == up) { cand[lo2] = y; cand[hi2] = x; }
+      }
+      __syncthreads();
+    }
+  const int nh = nc < ha + hb ? nc : ha + hb;
+  for (int a = tid; a < nh; a += kThreads) {
+    const int r = (int)(unsigned)(cand[a] & 0xffffffffull);
+    hrow[a] = r;
+    unsigned h = ((unsigned)r * 2654435761u) & (kHotHash - 1);
+    while (atomicCAS(&hkey[h], -1, r) != -1) h = (h + 1) & (kHotHash - 1);
+    hslot[h] = a;
   }
-  const int nh = nhot < hmax ? nhot : hmax;
   const int na = nh < ha ? nh : ha, nb = nh - na;
-  // tier A is laid out [NW][na][q] (dense for the rows actually taken)
-  accB = accA + (size_t)NW * na * cols;
-  for (int t = tid; t < (NW * na + nb) * q; t += kThreads)
+  __syncthreads();
+  // tier A: [NW][na][q] private copies (dense for the rows actually taken)
+  for (int t = tid; t < NW * na * q; t += kThreads)
     reinterpret_cast<float4*>(accA)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
   float4* accw = reinterpret_cast<float4*>(accA) + (size_t)warp * na * q;
   const bool act = sub < per && gl < q;
@@ -806,10 +827,8 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
       for (int u = 0; u < U; ++u) {
         const int sv = row[u] >= 0 ? slot[u] : -1;
         if (row[u] >= 0 && sv < 0) red_add_v4(W + (row[u] * cols + 4 * gl), v[u]);
-        if (sv >= na) {
-          float* p = accB + (sv - na) * cols + 4 * gl;
-          atomicAdd(p, v[u].x); atomicAdd(p + 1, v[u].y); atomicAdd(p + 2, v[u].z); atomicAdd(p + 3, v[u].w);
-        }
+        if (sv >= na)   // tier B: one of kHotRep replica rows, by entry position
+          red_add_v4(rep + ((sv - na) * kHotRep + (k0 + u * per + sub) % kHotRep) * cols + 4 * gl, v[u]);
         const bool isA = sv >= 0 && sv < na;
         if (__any_sync(0xffffffffu, isA)) {
           for (int hs = 0; hs < per; ++hs) {
@@ -827,20 +846,32 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     rl = rn;
   }
   __syncthreads();
-  for (int t = tid; t < nh * q; t += kThreads) {
+  for (int t = tid; t < na * q; t += kThreads) {
     const int r = t / q, f = t - r * q;
-    float4 s;
-    if (r < na) {
-      const float4* a = reinterpret_cast<const float4*>(accA) + (size_t)r * q + f;
-      s = a[0];
-      for (int w = 1; w < NW; ++w) {
-        const float4 b = a[(size_t)w * na * q];
-        s.x += b.x; s.y += b.y; s.z += b.z; s.w += b.w;
-      }
-    } else {
-      s = reinterpret_cast<const float4*>(accB)[(size_t)(r - na) * q + f];
+    const float4* a = reinterpret_cast<const float4*>(accA) + (size_t)r * q + f;
+    float4 sm4 = a[0];
+    for (int w = 1; w < NW; ++w) {
+      const float4 b = a[(size_t)w * na * q];
+      sm4.x += b.x; sm4.y += b.y; sm4.z += b.z; sm4.w += b.w;
     }
-    red_add_v4(W + (size_t)hrow[r] * cols + 4 * f, s);
+    red_add_v4(W + (size_t)hrow[r] * cols + 4 * f, sm4);
+  }
+  if (nb == 0) return;   // identical in every CTA (same sample, same ranking)
+  // tier B: after every CTA's reductions have landed, CTA c folds replica
+  // rows j = c, c + grid, ... into W and clears them for the next call
+  grid_barrier(&st->hot_arrivals);
+  for (int t = blockIdx.x * kThreads + tid; t < nb * q; t += gridDim.x * kThreads) {
+    const int j = t / q, f = t - j * q;
+    float4* r4 = reinterpret_cast<float4*>(rep + (size_t)j * kHotRep * cols) + f;
+    float4 sm4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < kHotRep; ++r) {
+      const float4 b = __ldcg(r4 + (size_t)r * q);
+      sm4.x += b.x; sm4.y += b.y; sm4.z += b.z; sm4.w += b.w;
+    }
+#pragma unroll
+    for (int r = 0; r < kHotRep; ++r) __stcg(r4 + (size_t)r * q, make_float4(0.f, 0.f, 0.f, 0.f));
+    red_add_v4(W + (size_t)hrow[na + j] * cols + 4 * f, sm4);
   }
 }
 
@@ -892,14 +923,13 @@ constexpr size_t kHotSmemMax = 200 * 1024;
 // rows if the warps' copies fit in 2/3 of the budget, tier B the rest (<= kHotB).
 static void hot_tiers(int cols, int* ha, int* hb) {
   const size_t row = sizeof(float) * cols, nw = kHotThreads / 32;
-  int a = (int)((kHotSmemMax * 2 / 3) / (nw * row));
+  int a = (int)(kHotSmemMax / (nw * row));
   *ha = a > 32 ? 32 : a;
-  int b = (int)((kHotSmemMax - (size_t)*ha * nw * row) / row);
-  *hb = b > kHotB ? kHotB : b;
+  *hb = kHotB;   // tier B lives in global replica rows (ScatterPlan::off_rep)
 }
-static size_t hot_smem(int ha, int hb, int cols) {
-  const size_t acc = sizeof(float) * ((size_t)(kHotThreads / 32) * ha + hb) * cols;
-  const size_t samp = sizeof(int) * 2 * kHotSampleHash;
+static size_t hot_smem(int ha, int cols) {
+  const size_t acc = sizeof(float) * (size_t)(kHotThreads / 32) * ha * cols;
+  const size_t samp = sizeof(int) * 2 * kHotSampleHash + sizeof(unsigned long long) * kHotCand;
   return acc > samp ? acc : samp;
 }
 static bool g_sort_coop_ok = false;   // sc_sort_coop fits 1 CTA/SM (scatter_prepare)
@@ -922,6 +952,9 @@ ScatterPlan scatter_plan(int64_t rows, int cols, int64_t n, int num_sms) {
   auto take = [&](size_t b) { size_t r = o; o += (b + 255) & ~size_t(255); return r; };
   pl.off_status = take(sizeof(ScatterStatus));
   pl.zero_bytes = o;   // only the status block is reset per call
+  // ATOMIC tier-B replica rows: kept zero between calls by the kernel itself;
+  // at a fixed offset (right after the status) for every plan
+  pl.off_rep = take(sizeof(float) * kHotB * kHotRep * 128);
   pl.off_hist = take(sizeof(int) * pl.bins * pl.ntiles);   // digit-major tile counts
   pl.off_ctr = take(sizeof(int) * (kScanBlocks > 1024 ? kScanBlocks : 1024));   // scan partials / digit totals
   pl.off_lookback = take(16);
@@ -964,10 +997,11 @@ cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t ro
   if (mode == 1 && (cols & 3) == 0 && cols <= 128 && rows * cols < (1ll << 31) && n * cols < (1ll << 31)) {
     int ha, hb;
     hot_tiers(cols, &ha, &hb);
-    const size_t smem = hot_smem(ha, hb, cols);
+    const size_t smem = hot_smem(ha, cols);
     int par = (int)(epoch & 1);
+    float* rep = reinterpret_cast<float*>(b + pl.off_rep);
     void* args[] = {(void*)&I, (void*)&Y, (void*)&W, (void*)&rows, (void*)&cols, (void*)&n,
-                    (void*)&ha, (void*)&hb, (void*)&st, (void*)&par};
+                    (void*)&ha, (void*)&hb, (void*)&st, (void*)&par, (void*)&rep};
     *launches += 1;
     *slot = par;
     return cudaLaunchCooperativeKernel(kHotFn, pl.num_sms, kHotThreads, args, smem, s);

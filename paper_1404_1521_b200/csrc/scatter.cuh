@@ -23,7 +23,7 @@ struct ScatterPlan {
   int passes, bits, bins, num_sms;
   int64_t ntiles, nchunks;
   size_t off_status, off_hist, off_ctr, off_lookback, zero_bytes;
-  size_t off_ka, off_va, off_kb, off_vb, off_carry, off_cfk, off_clk, total_bytes;
+  size_t off_ka, off_va, off_kb, off_vb, off_carry, off_cfk, off_clk, off_rep, total_bytes;
 };
 
 ScatterPlan scatter_plan(int64_t rows, int cols, int64_t n, int num_sms);
