@@ -161,10 +161,13 @@ pg_status pg_sync(pg_model* m);
  * k order within fixed-size chunks, chunk partials combined in chunk order:
  * bit-reproducible run to run (cols in {1..32, 64, 128}).  mode
  * PG_SCATTER_ATOMIC: one streaming pass over Y; the rows that a fixed
- * strided sample of I shows to be frequent (>~0.05 % of entries) are summed in
- * shared memory per CTA, every other entry reaches W through
+ * strided sample of I shows to be frequent (>~0.1 % of entries) are summed in
+ * shared memory per CTA (the most frequent) or spread over replica rows in the
+ * library's workspace, every other entry reaches W through
  * red.global.add.v4.f32 per 16 B (cols % 4 == 0, cols <= 128; other widths
  * use scalar atomics); the summation order is not fixed.
+ * Both modes use one library workspace per device: calls on the same device
+ * must not overlap in time on different streams.
  * W and Y must be 16-byte aligned (cudaMalloc memory is), else PG_EINVAL.
  * n == 0 is a no-op.  Out-of-range I[k] -> PG_ERANGE and W unchanged.
  * stream: a cudaStream_t (NULL = legacy default).  Blocking (it reports the
