@@ -804,7 +804,7 @@ static pg_status scatter_common(float* W, int64_t rows, int32_t cols, const floa
   CU(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   const int flag = slot < 0 ? hs.flag : hs.hot[slot].flag;
-  const unsigned long long bad = slot < 0 ? hs.bad : ~hs.hot[slot].nbad;
+  const unsigned long long bad = slot < 0 ? ~hs.nbad : ~hs.hot[slot].nbad;
   if (flag) {
     return fail(PG_ERANGE, "pg_scatter_add: index out of range at position %lld (value %d); W unchanged",
                 (long long)(bad >> 32), (int)(unsigned)(bad & 0xffffffffull));

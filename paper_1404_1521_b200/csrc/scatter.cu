@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kSortThreads) sc_upsweep(const int32_t* __rest
     const bool valid = e < n;
     int k = key[j];
     if (valid && rows > 0 && (k < 0 || (int64_t)k >= rows)) {
-      atomicMin(&st->bad, ((unsigned long long)e << 32) | (unsigned)k);
+      atomicMax(&st->nbad, ~(((unsigned long long)e << 32) | (unsigned)k));
       atomicOr(&st->flag, 1);
       k = 0;
     }
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kSortThreads) sc_sort_coop(
       const int64_t e = base + j * 32 + lane;
       const bool valid = e < n;
       if (p == 0 && valid && (keys[j] < 0 || (int64_t)keys[j] >= rows)) {
-        atomicMin(&st->bad, ((unsigned long long)e << 32) | (unsigned)keys[j]);
+        atomicMax(&st->nbad, ~(((unsigned long long)e << 32) | (unsigned)keys[j]));
         atomicOr(&st->flag, 1);
         keys[j] = 0;
       }
@@ -620,7 +620,7 @@ __global__ void sc_validate(const int32_t* __restrict__ I, int64_t n, int64_t ro
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
     const int key = __ldg(I + e);
     if (key < 0 || (int64_t)key >= rows) {
-      atomicMin(&st->bad, ((unsigned long long)e << 32) | (unsigned)key);
+      atomicMax(&st->nbad, ~(((unsigned long long)e << 32) | (unsigned)key));
       atomicOr(&st->flag, 1);
     }
   }
@@ -1007,8 +1007,6 @@ cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t ro
     return cudaLaunchCooperativeKernel(kHotFn, pl.num_sms, kHotThreads, args, smem, s);
   }
   e = cudaMemsetAsync(b, 0, pl.zero_bytes, s);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(&st->bad, 0xff, sizeof(st->bad), s);   // "no bad index"
   if (e != cudaSuccess) return e;
   const int blocks = pl.num_sms * 4;
   if (mode == 1) {

@@ -9,7 +9,7 @@ namespace pg {
 struct ScatterStatus {
   int flag;                 // 1: an index was out of range -> nothing applied
   int pad;
-  unsigned long long bad;   // min over (position << 32 | uint32 value)
+  unsigned long long nbad;  // max over ~(position << 32 | uint32 value): 0 = no bad index, so one memset resets the block
   unsigned long long arrivals;   // grid-barrier counter of the cooperative kernels
   // sc_atomic_hot (no per-call memset): call e uses hot[e & 1] and clears
   // hot[(e + 1) & 1] for the next call; nbad = ~(position << 32 | value),
