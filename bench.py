@@ -331,7 +331,7 @@ def main():
             "peaks": {"source": peak_kind, "hbm_gbs": peaks.get("hbm_gbs")},
         }
         out.update(extras)
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:   # the oracle's host baseline: N = 1 only
             rate, dt = oracle_rate(1024, 25)
             out["cpu_baseline"] = {"value": rate, "unit": "examples/s", "cores": 1, "kind": "oracle",
                                    "sample": "25 SGD steps x batch 1024 (Polyglot shape), float64, 1 host thread"}
