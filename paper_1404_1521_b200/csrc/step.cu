@@ -1177,14 +1177,21 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
           }
           const int L = lo;
           const int rel = base + e - lbase[L];   // offset inside the owner bucket (< 256)
-          const unsigned row = (unsigned)__ldcg(p.list_rows + list_index(p, L, loff[L] + rel));
-          keys[e] = ((unsigned long long)row << 32) | ((unsigned long long)L << 8) | (unsigned)rel;
+          // low word: the entry's position in the list storage, which grows
+          // with (list, offset) in both layouts (per-CTA lists; DP records,
+          // rank-major with compacted owner buckets), so sorting by the key
+          // orders each row's entries by (list, offset) as before
+          const size_t li = list_index(p, L, loff[L] + rel);
+          const unsigned row = (unsigned)__ldcg(p.list_rows + li);
+          keys[e] = ((unsigned long long)row << 32) | (unsigned long long)(unsigned)li;
         } else {
           keys[e] = ~0ull;
         }
       }
       __syncthreads();
+      trace_mark(p, 40);
       bitonic_sort(keys, npow);
+      trace_mark(p, 41);
       int nseg_total = 0;
       #pragma unroll 1
       for (int e0 = 0; e0 < Mw; e0 += NT) {
@@ -1198,30 +1205,29 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
       }
       if (tid == 0) seg[nseg_total] = Mw;
       __syncthreads();
+      trace_mark(p, 42);
       int par = 0;   // carry double buffer: read carry[par], write carry[par ^ 1]
       #pragma unroll 1
       for (int sb0 = 0; sb0 < Mw; sb0 += lay.SB, par ^= 1) {
         const int sb1 = min(Mw, sb0 + lay.SB);
         if ((d & 3) == 0) {   // 16 B pieces
           const int Q = d >> 2;
-          #pragma unroll 4
+          #pragma unroll 8
           for (int t = tid; t < (sb1 - sb0) * Q; t += NT) {
             const int e = sb0 + t / Q, f = t - (t / Q) * Q;
-            const unsigned long long k = keys[e];
-            const int L = (int)((k >> 8) & 0xffffff), rel = (int)(k & 0xff);
-            reinterpret_cast<float4*>(stage)[t] =
-                __ldcg(reinterpret_cast<const float4*>(p.list_vals + list_index(p, L, loff[L] + rel) * d) + f);
+            const size_t li = (unsigned)keys[e];
+            reinterpret_cast<float4*>(stage)[t] = __ldcg(reinterpret_cast<const float4*>(p.list_vals + li * d) + f);
           }
         } else {
           #pragma unroll 1
           for (int t = tid; t < (sb1 - sb0) * d; t += NT) {
             const int e = sb0 + t / d, f = t % d;
-            const unsigned long long k = keys[e];
-            const int L = (int)((k >> 8) & 0xffffff), rel = (int)(k & 0xff);
-            stage[t] = __ldcg(p.list_vals + list_index(p, L, loff[L] + rel) * d + f);
+            const size_t li = (unsigned)keys[e];
+            stage[t] = __ldcg(p.list_vals + li * d + f);
           }
         }
         __syncthreads();
+        if (sb0 == 0) trace_mark(p, 44);
         int slo = 0, shi = nseg_total - 1;
         while (slo < shi) {
           int mid = (slo + shi + 1) >> 1;
@@ -1302,10 +1308,12 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
           }
         }
         __syncthreads();
+        if (sb0 == 0) trace_mark(p, 45);
       }
     }
     La = Lb;
   }
+  trace_mark(p, 43);
 }
 
 // Trip 1 of the owner merge: CTA q's entry count in every list, scanned into

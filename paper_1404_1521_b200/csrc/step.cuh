@@ -139,7 +139,7 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   o = p2fixed;
   L.keys = o;  o = align16(o + kCapK * 8);
   L.seg = o;   o = align16(o + (kCapK + 1) * 4);
-  int SB = 65536 / (d * 4);
+  int SB = 131072 / (d * 4);   // fallback window: 512 entries at d = 64
   if (SB > 512) SB = 512;
   if (SB < 16) SB = 16;
   L.SB = SB;

@@ -68,6 +68,11 @@ print("slowest CTAs (last step): cta end_us M | trip2 hash scan trip3 sums (us)"
 for b in slow:
     st = [(x[b, k2] - x[b, k1]) / 1e3 for k1, k2 in ((20, 21), (21, 22), (22, 23), (23, 24), (24, 11))]
     print(f"  {b:4d} {ends[b]:6.2f} {int(x[b, 31]):4d} | " + " ".join(f"{v:5.2f}" for v in st))
+    if x[b, 43] > 0:   # sorted fallback stamps: keys built, sorted, segments, windows done
+        print("       fallback: start->keys {:5.2f} sort {:5.2f} segs {:5.2f} windows {:5.2f} | after {:5.2f}".format(
+            (x[b, 40] - x[b, 29]) / 1e3, (x[b, 41] - x[b, 40]) / 1e3, (x[b, 42] - x[b, 41]) / 1e3,
+            (x[b, 43] - x[b, 42]) / 1e3, (x[b, 11] - x[b, 43]) / 1e3))
+        print("       first window: stage {:5.2f} sums {:5.2f}".format((x[b, 44] - x[b, 42]) / 1e3, (x[b, 45] - x[b, 44]) / 1e3))
 med = np.median(X[-1][:, 31])
 print(f"median M {med:.0f}, max M {X[-1][:, 31].max():.0f}")
 
