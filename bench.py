@@ -137,15 +137,18 @@ def load_traffic():
 
 
 # ---------------------------------------------------------------------- oracle (reference arm / cpu baseline)
-def oracle_rate(B, steps, seed=42):
-    """The float64 oracle as it stands, single host thread, on `steps` Polyglot steps."""
+def oracle_rate(B, steps, seed=42, warmup=0):
+    """The float64 oracle as it stands, single host thread, on `steps` Polyglot
+    steps (after `warmup` untimed ones)."""
     import oracle
     import synth
     V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
     p = oracle.Params.init(V, d, n, h, seed)
-    batches = [synth.batch(V, n, B, seed=seed, step=t) for t in range(steps)]
+    batches = [synth.batch(V, n, B, seed=seed, step=t) for t in range(warmup + steps)]
+    for idx, corr in batches[:warmup]:
+        oracle.train_step(p, idx, corr, 0.1)
     t0 = time.perf_counter()
-    for idx, corr in batches:
+    for idx, corr in batches[warmup:]:
         oracle.train_step(p, idx, corr, 0.1)
     dt = time.perf_counter() - t0
     return B * steps / dt, dt
@@ -155,15 +158,18 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 20))
+    # each step: one oracle SGD step on a bounded sample (batch <= 1024, ~50 ms)
+    steps = max(1, min(args.steps, 200))
+    warm = max(0, min(args.warmup, 5))
     B = min(args.batch, 1024)
-    rate, dt = oracle_rate(B, steps)
+    rate, dt = oracle_rate(B, steps, warmup=warm)
     cfg = {"workload": f"polyglot_v100k_d64_n5_h32_b{args.batch}", "vocab": POLY["V"], "dim": POLY["d"],
            "window": POLY["n"], "hidden": POLY["h"], "batch_per_gpu": args.batch,
            "oracle_sample": f"{steps} steps x batch {B}"}
     print(json.dumps({
         "impl": "reference", "metric": "training examples/sec", "value": rate, "unit": "examples/s",
-        "n_gpus": 0, "steps": steps, "warmup": 0, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
+        "n_gpus": args.gpus, "device": "host cpu (1 thread)", "steps": steps, "warmup": warm,
+        "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": rate, "unit": "examples/s", "cores": 1, "kind": "oracle",
                          "sample": f"{steps} SGD steps of batch {B} (Polyglot shape), float64, 1 thread"},
