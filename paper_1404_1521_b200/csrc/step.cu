@@ -1210,13 +1210,24 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
       #pragma unroll 1
       for (int sb0 = 0; sb0 < Mw; sb0 += lay.SB, par ^= 1) {
         const int sb1 = min(Mw, sb0 + lay.SB);
-        if ((d & 3) == 0) {   // 16 B pieces
-          const int Q = d >> 2;
-          #pragma unroll 8
-          for (int t = tid; t < (sb1 - sb0) * Q; t += NT) {
-            const int e = sb0 + t / Q, f = t - (t / Q) * Q;
-            const size_t li = (unsigned)keys[e];
-            reinterpret_cast<float4*>(stage)[t] = __ldcg(reinterpret_cast<const float4*>(p.list_vals + li * d) + f);
+        if ((d & 3) == 0) {   // 16 B pieces, 8 loads in flight per thread
+          const int Q = d >> 2, nq = (sb1 - sb0) * Q;
+          float4* st4w = reinterpret_cast<float4*>(stage);
+          #pragma unroll 1
+          for (int t0 = tid; t0 < nq; t0 += 8 * NT) {
+            float4 v[8];
+            #pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int t = t0 + j * NT;
+              if (t < nq) {
+                const int e = sb0 + t / Q, f = t - (t / Q) * Q;
+                const size_t li = (unsigned)keys[e];
+                v[j] = __ldcg(reinterpret_cast<const float4*>(p.list_vals + li * d) + f);
+              }
+            }
+            #pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (t0 + j * NT < nq) st4w[t0 + j * NT] = v[j];
           }
         } else {
           #pragma unroll 1
@@ -1228,87 +1239,107 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
         }
         __syncthreads();
         if (sb0 == 0) trace_mark(p, 44);
+        if (sb0 / lay.SB < 4) trace_mark(p, 50 + 2 * (sb0 / lay.SB));
         int slo = 0, shi = nseg_total - 1;
         while (slo < shi) {
           int mid = (slo + shi + 1) >> 1;
           if (seg[mid] <= sb0) slo = mid; else shi = mid - 1;
         }
-        if ((d & 3) == 0) {
-          // thread per (segment, float4): 4 fixed chains by the entry's offset
-          // from its segment start (so a long, hot segment is summed with 4-way
-          // ILP by d/4 threads instead of serially by one warp), combined as
-          // (c0 + c1) + (c2 + c3); a segment crossing the window end hands its
-          // 4 chains on through `carry` [2][4][d/4] float4.
-          int she = slo, hi2 = nseg_total;   // first segment starting at or after sb1
-          while (she < hi2) {
-            const int mid = (she + hi2) >> 1;
-            if (seg[mid] < sb1) she = mid + 1; else hi2 = mid;
+        int she = slo, hi2 = nseg_total;   // first segment starting at or after sb1
+        while (she < hi2) {
+          const int mid = (she + hi2) >> 1;
+          if (seg[mid] < sb1) she = mid + 1; else hi2 = mid;
+        }
+        // thread per (segment, column): 4 fixed chains by the entry's offset
+        // from its segment start, combined as (c0 + c1) + (c2 + c3), so a long
+        // (hot) segment is summed by d threads with 4-way ILP; a segment
+        // crossing the window end hands its chains on through `carry` [2][4][d]
+        const int nsw = she - slo;
+        #pragma unroll 1
+        for (int it = tid; it < nsw * d; it += NT) {
+          const int sidx = slo + it / d, f = it - (it / d) * d;
+          const int s0 = seg[sidx], s1 = seg[sidx + 1];
+          const int a0 = max(s0, sb0), a1 = min(s1, sb1);
+          const bool cont = s0 < sb0, fin = s1 <= sb1;
+          float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+          if (cont) {
+            c0 = carry[(par * 4 + 0) * d + f]; c1 = carry[(par * 4 + 1) * d + f];
+            c2 = carry[(par * 4 + 2) * d + f]; c3 = carry[(par * 4 + 3) * d + f];
           }
-          const int Q = d >> 2, nsw = she - slo;
-          const float4* st4 = reinterpret_cast<const float4*>(stage);
-          float4* cr4 = reinterpret_cast<float4*>(carry);
+          // stage[(e - sb0) * d + f] walked with a running index (shared-space
+          // addressing), 4 chains by (e - s0) & 3
+          int ix = (a0 - sb0) * d + f;
+          int e = a0;
+          for (; e < a1 && ((e - s0) & 3); ++e, ix += d) {
+            const float v = stage[ix];
+            const int k = (e - s0) & 3;
+            if (k == 0) c0 += v; else if (k == 1) c1 += v; else if (k == 2) c2 += v; else c3 += v;
+          }
+          const int d4 = 4 * d;
+          #pragma unroll 4
+          for (; e + 3 < a1; e += 4, ix += d4) {
+            c0 += stage[ix]; c1 += stage[ix + d]; c2 += stage[ix + 2 * d]; c3 += stage[ix + 3 * d];
+          }
+          for (; e < a1; ++e, ix += d) {
+            const float v = stage[ix];
+            const int k = (e - s0) & 3;
+            if (k == 0) c0 += v; else if (k == 1) c1 += v; else if (k == 2) c2 += v; else c3 += v;
+          }
+          if (fin) {   // total parked in the segment's first staged row (dead now)
+            stage[(size_t)(a0 - sb0) * d + f] = (c0 + c1) + (c2 + c3);
+          } else {
+            carry[((par ^ 1) * 4 + 0) * d + f] = c0; carry[((par ^ 1) * 4 + 1) * d + f] = c1;
+            carry[((par ^ 1) * 4 + 2) * d + f] = c2; carry[((par ^ 1) * 4 + 3) * d + f] = c3;
+          }
+        }
+        __syncthreads();
+        if (sb0 / lay.SB < 4) trace_mark(p, 51 + 2 * (sb0 / lay.SB));
+        // C += -lr * total for the segments that end in this window, with
+        // several row reads in flight per thread (not one dependent global
+        // round trip per (segment, column))
+        {
+          const int fin0 = (nsw > 0 && seg[she] > sb1) ? she - 1 : she;   // segments [slo, fin0) end here
+          const int nfin = fin0 - slo;
+          const bool v4 = (d & 3) == 0;
+          const int W4 = v4 ? d >> 2 : d;
           #pragma unroll 1
-          for (int it = tid; it < nsw * Q; it += NT) {
-            const int sidx = slo + it / Q, qf = it - (it / Q) * Q;
-            const int s0 = seg[sidx], s1 = seg[sidx + 1];
-            const int a0 = max(s0, sb0), a1 = min(s1, sb1);
-            const bool cont = s0 < sb0, fin = s1 <= sb1;
-            float4 c[4];
+          for (int t0 = tid; t0 < nfin * W4; t0 += 4 * NT) {
+            float4 cur[4];
+            float4* dst[4];
+            float4 tot[4];
             #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              c[k] = cont ? cr4[(par * 4 + k) * Q + qf] : make_float4(0.f, 0.f, 0.f, 0.f);
-            auto add = [&](int k, float4 v) {
-              #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                if (kk == k) { c[kk].x += v.x; c[kk].y += v.y; c[kk].z += v.z; c[kk].w += v.w; }
-            };
-            int e = a0;
-            for (; e < a1 && ((e - s0) & 3); ++e) add((e - s0) & 3, st4[(e - sb0) * Q + qf]);
-            #pragma unroll 2
-            for (; e + 3 < a1; e += 4) {
-              const float4 v0 = st4[(e - sb0) * Q + qf], v1 = st4[(e + 1 - sb0) * Q + qf];
-              const float4 v2 = st4[(e + 2 - sb0) * Q + qf], v3 = st4[(e + 3 - sb0) * Q + qf];
-              add(0, v0); add(1, v1); add(2, v2); add(3, v3);
-            }
-            for (; e < a1; ++e) add((e - s0) & 3, st4[(e - sb0) * Q + qf]);
-            if (fin) {
-              const unsigned row = (unsigned)(keys[s0] >> 32);
-              float4 t;
-              t.x = (c[0].x + c[1].x) + (c[2].x + c[3].x);
-              t.y = (c[0].y + c[1].y) + (c[2].y + c[3].y);
-              t.z = (c[0].z + c[1].z) + (c[2].z + c[3].z);
-              t.w = (c[0].w + c[1].w) + (c[2].w + c[3].w);
-              float4* cp = reinterpret_cast<float4*>(p.C + (size_t)row * d) + qf;
-              const float4 o = __ldcg(cp);
-              *cp = make_float4(o.x + nlr * t.x, o.y + nlr * t.y, o.z + nlr * t.z, o.w + nlr * t.w);
-            } else {
-              #pragma unroll
-              for (int k = 0; k < 4; ++k) cr4[((par ^ 1) * 4 + k) * Q + qf] = c[k];
-            }
-          }
-        } else {
-          #pragma unroll 1
-          for (int sidx = slo + warp; sidx < nseg_total && seg[sidx] < sb1; sidx += NW) {
-            const int s0 = seg[sidx], s1 = seg[sidx + 1];
-            const int a0 = max(s0, sb0), a1 = min(s1, sb1);
-            const bool cont = s0 < sb0, fin = s1 <= sb1;
-            const unsigned row = (unsigned)(keys[s0] >> 32);
-            #pragma unroll 1
-            for (int f = lane; f < d; f += 32) {
-              float acc = cont ? carry[par * d + f] : 0.f;
-              #pragma unroll 1
-              for (int e = a0; e < a1; ++e) acc += stage[(e - sb0) * d + f];
-              if (fin) {
-                float* cp = p.C + (size_t)row * d + f;
-                *cp = __ldcg(cp) + nlr * acc;
-              } else {
-                carry[(par ^ 1) * d + f] = acc;
+            for (int j = 0; j < 4; ++j) {
+              const int t = t0 + j * NT;
+              dst[j] = nullptr;
+              if (t < nfin * W4) {
+                const int sidx = slo + t / W4, f = t - (t / W4) * W4;
+                const int a0 = max(seg[sidx], sb0);
+                const unsigned row = (unsigned)(keys[seg[sidx]] >> 32);
+                if (v4) {
+                  dst[j] = reinterpret_cast<float4*>(p.C + (size_t)row * d) + f;
+                  tot[j] = reinterpret_cast<const float4*>(stage + (size_t)(a0 - sb0) * d)[f];
+                  cur[j] = __ldcg(dst[j]);
+                } else {
+                  dst[j] = reinterpret_cast<float4*>(p.C + (size_t)row * d + f);   // scalar slot
+                  tot[j].x = stage[(size_t)(a0 - sb0) * d + f];
+                  cur[j].x = __ldcg(p.C + (size_t)row * d + f);
+                }
               }
+            }
+            #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (!dst[j]) continue;
+              if (v4)
+                *dst[j] = make_float4(cur[j].x + nlr * tot[j].x, cur[j].y + nlr * tot[j].y,
+                                      cur[j].z + nlr * tot[j].z, cur[j].w + nlr * tot[j].w);
+              else
+                *reinterpret_cast<float*>(dst[j]) = cur[j].x + nlr * tot[j].x;
             }
           }
         }
         __syncthreads();
         if (sb0 == 0) trace_mark(p, 45);
+        if (sb0 / lay.SB < 4) trace_mark(p, 46 + sb0 / lay.SB);
       }
     }
     La = Lb;

@@ -73,6 +73,8 @@ for b in slow:
             (x[b, 40] - x[b, 29]) / 1e3, (x[b, 41] - x[b, 40]) / 1e3, (x[b, 42] - x[b, 41]) / 1e3,
             (x[b, 43] - x[b, 42]) / 1e3, (x[b, 11] - x[b, 43]) / 1e3))
         print("       first window: stage {:5.2f} sums {:5.2f}".format((x[b, 44] - x[b, 42]) / 1e3, (x[b, 45] - x[b, 44]) / 1e3))
+        print("       window ends (us after segs):", " ".join("{:5.2f}".format((x[b, k] - x[b, 42]) / 1e3) for k in range(46, 50) if x[b, k] > 0))
+        print("       per window staged / summed (us after segs):", " ".join("{:5.2f}".format((x[b, k] - x[b, 42]) / 1e3) for k in range(50, 58) if x[b, k] > 0))
 med = np.median(X[-1][:, 31])
 print(f"median M {med:.0f}, max M {X[-1][:, 31].max():.0f}")
 
