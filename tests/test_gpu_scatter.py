@@ -184,3 +184,16 @@ def test_atomic_hot_rows_int_payload_bitwise(env, cols):
     Y = rng.integers(-8, 9, (n, cols)).astype(np.float32)
     ref = oracle.index_add(np.zeros((rows, cols), np.float32), Y, I)
     assert np.array_equal(gpu_scatter(env, np.zeros((rows, cols), np.float32), Y, I, 1), ref)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("cols", [1, 5, 30])
+def test_odd_widths_int_payload_bitwise(env, mode, cols):
+    """Widths that are not a multiple of 4 (scalar paths) with integer payloads
+    and Zipf-repeated rows: bitwise equal to the serial oracle."""
+    rng = np.random.default_rng(100 + cols)
+    rows, n = 3000, 50_000
+    I = (rng.zipf(1.2, n) % rows).astype(np.int32)
+    Y = rng.integers(-8, 9, (n, cols)).astype(np.float32)
+    ref = oracle.index_add(np.zeros((rows, cols), np.float32), Y, I)
+    assert np.array_equal(gpu_scatter(env, np.zeros((rows, cols), np.float32), Y, I, mode), ref)
