@@ -826,9 +826,10 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
         pre[k] = (rr < nA && has_u && !first) ? __ldcg(reinterpret_cast<const float4*>(rec + (size_t)rr * h) + lane)
                                               : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+      int sl = warp / d, j = warp - (warp / d) * d;   // (slot, feature) of row rr, stepped without a division
 #pragma unroll 1
-      for (int rr = warp; rr < nA; rr += NW) {
-        const int sl = rr / d, j = rr - sl * d;
+      for (int rr = warp; rr < nA; rr += NW, j += NW) {
+        while (j >= d) { j -= d; ++sl; }
         const int cls = sl == c ? 1 : 0;
         if (cls != cur_cls) {
           cur_cls = cls;
