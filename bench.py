@@ -243,6 +243,8 @@ def main():
         tot_ms = float(tt.item())
     ms_per_step = tot_ms / args.steps
     value = B * world * args.steps / (tot_ms / 1e3)
+    step_stats = {"median_ms": statistics.median(times), "min_ms": min(times), "max_ms": max(times),
+                  "pstdev_ms": statistics.pstdev(times), "rank": rank}   # this rank's K event-timed steps
 
     # ---- warm-L2 steady state: K steps back to back (table stays L2-resident)
     with torch.cuda.stream(stream):
@@ -319,7 +321,8 @@ def main():
         tr = load_traffic().get(f"step_b{B}")
         out = {
             "metric": "training examples/sec", "value": value, "unit": "examples/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "step_stats": step_stats,
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"polyglot_v100k_d64_n5_h32_b{B}", "vocab": V, "dim": d, "window": n,
                        "hidden": h, "batch_per_gpu": B, "global_batch": B * world,
