@@ -1144,6 +1144,51 @@ __device__ void bitonic_sort(unsigned long long* k, int n) {
   }
 }
 
+// One (segment, column) work item of the sorted fallback's window sums: the
+// segment's entries [max(s0, sb0), min(s1, sb1)) of staged column `col`
+// (units of VT: float or float4) summed in 4 chains by (e - s0) & 3, combined
+// as (c0 + c1) + (c2 + c3); a finished segment parks its total in its first
+// staged row, a window-crossing one hands its chains on through `carry`
+// [2][4][d] floats (the same bytes for either VT).
+__device__ __forceinline__ float vzero(float) { return 0.f; }
+__device__ __forceinline__ float4 vzero(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void vadd(float& a, float b) { a += b; }
+__device__ __forceinline__ void vadd(float4& a, float4 b) { a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w; }
+template <typename VT>
+__device__ __forceinline__ void fb_segsum(float* stage, float* carry, int d, int sb0, int sb1, int s0, int s1,
+                                          int col, int par) {
+  constexpr int VW = sizeof(VT) / sizeof(float);
+  const int rs = d / VW;   // row stride in VT units
+  VT* st = reinterpret_cast<VT*>(stage);
+  VT* cr = reinterpret_cast<VT*>(carry);
+  const int a0 = max(s0, sb0), a1 = min(s1, sb1);
+  VT c0 = vzero(VT()), c1 = c0, c2 = c0, c3 = c0;
+  if (s0 < sb0) {
+    c0 = cr[(par * 4 + 0) * rs + col]; c1 = cr[(par * 4 + 1) * rs + col];
+    c2 = cr[(par * 4 + 2) * rs + col]; c3 = cr[(par * 4 + 3) * rs + col];
+  }
+  int ix = (a0 - sb0) * rs + col, e = a0;
+  for (; e < a1 && ((e - s0) & 3); ++e, ix += rs) {
+    const int k = (e - s0) & 3;
+    if (k == 0) vadd(c0, st[ix]); else if (k == 1) vadd(c1, st[ix]); else if (k == 2) vadd(c2, st[ix]); else vadd(c3, st[ix]);
+  }
+  #pragma unroll 4
+  for (; e + 3 < a1; e += 4, ix += 4 * rs) {
+    vadd(c0, st[ix]); vadd(c1, st[ix + rs]); vadd(c2, st[ix + 2 * rs]); vadd(c3, st[ix + 3 * rs]);
+  }
+  for (; e < a1; ++e, ix += rs) {
+    const int k = (e - s0) & 3;
+    if (k == 0) vadd(c0, st[ix]); else if (k == 1) vadd(c1, st[ix]); else if (k == 2) vadd(c2, st[ix]); else vadd(c3, st[ix]);
+  }
+  if (s1 <= sb1) {
+    vadd(c0, c1); vadd(c2, c3); vadd(c0, c2);
+    st[(a0 - sb0) * rs + col] = c0;
+  } else {
+    cr[((par ^ 1) * 4 + 0) * rs + col] = c0; cr[((par ^ 1) * 4 + 1) * rs + col] = c1;
+    cr[((par ^ 1) * 4 + 2) * rs + col] = c2; cr[((par ^ 1) * 4 + 3) * rs + col] = c3;
+  }
+}
+
 // Sorted fallback for owners with more than MCAP entries (pathological index
 // patterns): windows of whole lists, bitonic sort by (row, list), segment sums
 // in list order with a carry across staged sub-batches.
@@ -1251,47 +1296,44 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
           const int mid = (she + hi2) >> 1;
           if (seg[mid] < sb1) she = mid + 1; else hi2 = mid;
         }
-        // thread per (segment, column): 4 fixed chains by the entry's offset
-        // from its segment start, combined as (c0 + c1) + (c2 + c3), so a long
-        // (hot) segment is summed by d threads with 4-way ILP; a segment
-        // crossing the window end hands its chains on through `carry` [2][4][d]
+        // window sums: short segments (<= kLongSeg entries here) by thread per
+        // (segment, float4) -- few items for many small segments -- long
+        // (hot) segments by thread per (segment, float column), d threads with
+        // 4-way ILP each; fb_segsum fixes the chain order, so the result does
+        // not depend on which form summed a segment
         const int nsw = she - slo;
+        constexpr int kLongSeg = 64;
+        int* longl = ws;   // <= SB / kLongSeg + 1 long segments per window
+        if (tid == 0) ws[63] = 0;
+        __syncthreads();
+        for (int i = tid; i < nsw; i += NT) {
+          const int s0 = seg[slo + i], s1 = seg[slo + i + 1];
+          if (min(s1, sb1) - max(s0, sb0) > kLongSeg) longl[atomicAdd(&ws[63], 1)] = slo + i;
+        }
+        __syncthreads();
+        const int nlong = ws[63];
+        if ((d & 3) == 0) {
+          const int Q = d >> 2;
+          #pragma unroll 1
+          for (int it = tid; it < nsw * Q; it += NT) {
+            const int sidx = slo + it / Q, qf = it - (it / Q) * Q;
+            const int s0 = seg[sidx], s1 = seg[sidx + 1];
+            if (min(s1, sb1) - max(s0, sb0) > kLongSeg) continue;
+            fb_segsum<float4>(stage, carry, d, sb0, sb1, s0, s1, qf, par);
+          }
+        } else {
+          #pragma unroll 1
+          for (int it = tid; it < nsw * d; it += NT) {
+            const int sidx = slo + it / d, f = it - (it / d) * d;
+            const int s0 = seg[sidx], s1 = seg[sidx + 1];
+            if (min(s1, sb1) - max(s0, sb0) > kLongSeg) continue;
+            fb_segsum<float>(stage, carry, d, sb0, sb1, s0, s1, f, par);
+          }
+        }
         #pragma unroll 1
-        for (int it = tid; it < nsw * d; it += NT) {
-          const int sidx = slo + it / d, f = it - (it / d) * d;
-          const int s0 = seg[sidx], s1 = seg[sidx + 1];
-          const int a0 = max(s0, sb0), a1 = min(s1, sb1);
-          const bool cont = s0 < sb0, fin = s1 <= sb1;
-          float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-          if (cont) {
-            c0 = carry[(par * 4 + 0) * d + f]; c1 = carry[(par * 4 + 1) * d + f];
-            c2 = carry[(par * 4 + 2) * d + f]; c3 = carry[(par * 4 + 3) * d + f];
-          }
-          // stage[(e - sb0) * d + f] walked with a running index (shared-space
-          // addressing), 4 chains by (e - s0) & 3
-          int ix = (a0 - sb0) * d + f;
-          int e = a0;
-          for (; e < a1 && ((e - s0) & 3); ++e, ix += d) {
-            const float v = stage[ix];
-            const int k = (e - s0) & 3;
-            if (k == 0) c0 += v; else if (k == 1) c1 += v; else if (k == 2) c2 += v; else c3 += v;
-          }
-          const int d4 = 4 * d;
-          #pragma unroll 4
-          for (; e + 3 < a1; e += 4, ix += d4) {
-            c0 += stage[ix]; c1 += stage[ix + d]; c2 += stage[ix + 2 * d]; c3 += stage[ix + 3 * d];
-          }
-          for (; e < a1; ++e, ix += d) {
-            const float v = stage[ix];
-            const int k = (e - s0) & 3;
-            if (k == 0) c0 += v; else if (k == 1) c1 += v; else if (k == 2) c2 += v; else c3 += v;
-          }
-          if (fin) {   // total parked in the segment's first staged row (dead now)
-            stage[(size_t)(a0 - sb0) * d + f] = (c0 + c1) + (c2 + c3);
-          } else {
-            carry[((par ^ 1) * 4 + 0) * d + f] = c0; carry[((par ^ 1) * 4 + 1) * d + f] = c1;
-            carry[((par ^ 1) * 4 + 2) * d + f] = c2; carry[((par ^ 1) * 4 + 3) * d + f] = c3;
-          }
+        for (int it = tid; it < nlong * d; it += NT) {
+          const int sidx = longl[it / d], f = it - (it / d) * d;
+          fb_segsum<float>(stage, carry, d, sb0, sb1, seg[sidx], seg[sidx + 1], f, par);
         }
         __syncthreads();
         if (sb0 / lay.SB < 4) trace_mark(p, 51 + 2 * (sb0 / lay.SB));
