@@ -192,8 +192,8 @@ struct Geometry {
 static Geometry geometry(const pg_model* m, int B) {
   Geometry g{};
   g.P = B < m->num_sms ? B : m->num_sms;
-  g.T = step_chunk_T(m->d, m->n, m->h, m->fast);
   const int per = (B + g.P - 1) / g.P;
+  g.T = step_chunk_T(m->d, m->n, m->h, m->fast, per);
   g.R = (per + g.T - 1) / g.T;
   g.cap = (m->n + 1) * g.T;
   g.NL = g.P * g.R;

@@ -633,7 +633,8 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
 
 // ------------------------------------------------------------------ TILED phase 1
 // d % 32 == 0, h % 32 == 0, 64 <= h <= 128 (the large config: d = h = 128):
-// chunks of kTT = 16 examples, 384 threads, every FMA an FFMA2 with one operand
+// chunks of kTT = 16 examples (kTTSmall = 4 when no CTA has more: step_kernel<3>),
+// 384 threads, every FMA an FFMA2 with one operand
 // broadcast, W1 read from L2 once per chunk per product (no per-thread
 // redundancy), all other operands from shared memory.
 //   forward  : thread (slot s, hidden pair) accumulates 16 examples over d
@@ -643,9 +644,11 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
 //              (its W1 row, sigma/delta/delta' as [u][e] float4 broadcasts);
 //   dW1      : thread (row, 32 hidden) accumulates over the 16 examples and
 //              adds into this CTA's dense record (CTA-private, chunk order).
-constexpr int kTT = 16;
-constexpr int kXTS = 20;   // XT row stride (floats): 16 examples + 4 pad, 16 B aligned
-__device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
+constexpr int kTT = 16;   // chunk size of the tiled path (kTTSmall when every CTA has <= 4 examples)
+constexpr int kTTSmall = 4;
+template <int TT>
+__device__ void phase1_tiled_t(const StepParams& p, unsigned char* sm) {
+  constexpr int XTS = TT + 4;   // XT row stride (floats): TT examples + 4 pad, 16 B aligned
   const Layout& lay = p.lay;
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
   const int d = p.d, n = p.n, h = p.h, E = n + 1, c = n >> 1, H2 = h >> 1;
@@ -667,19 +670,19 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
   float db1_acc = 0.f, dw2_acc = 0.f, hinge_acc = 0.f;   // thread u < h: db1[u], dw2[u]; thread 0: hinge
 #pragma unroll 1
   for (int r = 0; r < p.R; ++r) {
-    const long long e0 = lo + (long long)r * kTT;
-    const int cnt = (int)(hi - e0 < kTT ? (hi - e0 > 0 ? hi - e0 : 0) : kTT);
+    const long long e0 = lo + (long long)r * TT;
+    const int cnt = (int)(hi - e0 < TT ? (hi - e0 > 0 ? hi - e0 : 0) : TT);
     const int L = blockIdx.x * p.R + r;
     if (cnt <= 0) { write_empty_list(p, L); continue; }
     gather_rows(p, sm, e0, cnt, X, rows_s, r == 0, [] {}, [] {});
     // XT[s][j][e] = x of example e, slot s (slot n = corrupt centre); 0 past cnt.
     // Warp per (s, e), lanes over j: conflict-free row reads; the [j][e] rows are
-    // kXTS floats apart so the column writes are 4-way at worst.
+    // XTS floats apart so the column writes are 4-way at worst.
 #pragma unroll 1
-    for (int se = warp; se < E * kTT; se += NW) {
-      const int sl = se / kTT, e = se - sl * kTT;
+    for (int se = warp; se < E * TT; se += NW) {
+      const int sl = se / TT, e = se - sl * TT;
       const float* xr = X + (size_t)(e < cnt ? pu[e * E + sl] : 0) * d;
-      for (int j = lane; j < d; j += 32) XT[((size_t)sl * d + j) * kXTS + e] = e < cnt ? xr[j] : 0.f;
+      for (int j = lane; j < d; j += 32) XT[((size_t)sl * d + j) * XTS + e] = e < cnt ? xr[j] : 0.f;
     }
     __syncthreads();
     if (r < 2) trace_mark(p, 1 + 32 * r);
@@ -688,10 +691,10 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
     for (int it = tid; it < E * H2; it += NT) {
       const int sl = it / H2, pp = it - sl * H2, ws = sl == n ? c : sl;
       const float2* wc = reinterpret_cast<const float2*>(p.W1 + (size_t)ws * d * h) + pp;
-      const float4* xt = reinterpret_cast<const float4*>(XT + (size_t)sl * d * kXTS);
-      float2 acc[kTT];
+      const float4* xt = reinterpret_cast<const float4*>(XT + (size_t)sl * d * XTS);
+      float2 acc[TT];
 #pragma unroll
-      for (int e = 0; e < kTT; ++e) acc[e] = make_float2(0.f, 0.f);
+      for (int e = 0; e < TT; ++e) acc[e] = make_float2(0.f, 0.f);
       // every CTA reads the same W1; rotating the start row per CTA spreads the
       // simultaneous requests over the L2 slices instead of all CTAs hitting
       // the same lines in lockstep
@@ -701,8 +704,8 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
         const int j = jj + rot < d ? jj + rot : jj + rot - d;
         const float2 w = __ldg(wc + (size_t)j * H2);
 #pragma unroll
-        for (int q = 0; q < kTT / 4; ++q) {
-          const float4 x = xt[j * (kXTS / 4) + q];
+        for (int q = 0; q < TT / 4; ++q) {
+          const float4 x = xt[j * (XTS / 4) + q];
           acc[4 * q] = __ffma2_rn(w, make_float2(x.x, x.x), acc[4 * q]);
           acc[4 * q + 1] = __ffma2_rn(w, make_float2(x.y, x.y), acc[4 * q + 1]);
           acc[4 * q + 2] = __ffma2_rn(w, make_float2(x.z, x.z), acc[4 * q + 2]);
@@ -710,13 +713,13 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
         }
       }
 #pragma unroll
-      for (int e = 0; e < kTT; ++e) reinterpret_cast<float2*>(part + ((size_t)sl * kTT + e) * h)[pp] = acc[e];
+      for (int e = 0; e < TT; ++e) reinterpret_cast<float2*>(part + ((size_t)sl * TT + e) * h)[pp] = acc[e];
     }
     __syncthreads();
     if (r < 2) trace_mark(p, 2 + 32 * r);
     // ---- hinge, delta, delta', sigma: warp per example, lanes over h (<= 4 per lane)
 #pragma unroll 1
-    for (int e = warp; e < kTT; e += NW) {
+    for (int e = warp; e < TT; e += NW) {
       float a[4], ac[4], w2v[4];
       float sp = 0.f, spc = 0.f;
 #pragma unroll
@@ -726,9 +729,9 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
         if (u < h) {
           float ctx = __ldg(p.b1 + u);
           for (int sl = 0; sl < n; ++sl)
-            if (sl != c) ctx += part[((size_t)sl * kTT + e) * h + u];
-          a[k] = ctx + part[((size_t)c * kTT + e) * h + u];
-          ac[k] = ctx + part[((size_t)n * kTT + e) * h + u];
+            if (sl != c) ctx += part[((size_t)sl * TT + e) * h + u];
+          a[k] = ctx + part[((size_t)c * TT + e) * h + u];
+          ac[k] = ctx + part[((size_t)n * TT + e) * h + u];
           w2v[k] = __ldg(p.w2 + u);
           sp += w2v[k] * act_f(a[k], p.act);
           spc += w2v[k] * act_f(ac[k], p.act);
@@ -747,12 +750,12 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
           const float dl = act_g(g * w2v[k], a[k], z, p.act);
           const float dlc = act_g(-g * w2v[k], ac[k], zc, p.act);
           const float sg = act_sigma(g * w2v[k], z, zc, dl, dlc, p.act);
-          SU[((size_t)0 * h + u) * kXTS + e] = sg;
-          SU[((size_t)1 * h + u) * kXTS + e] = dl;
-          SU[((size_t)2 * h + u) * kXTS + e] = dlc;
-          SE[((size_t)0 * kTT + e) * h + u] = sg;
-          SE[((size_t)1 * kTT + e) * h + u] = dl;
-          SE[((size_t)2 * kTT + e) * h + u] = dlc;
+          SU[((size_t)0 * h + u) * XTS + e] = sg;
+          SU[((size_t)1 * h + u) * XTS + e] = dl;
+          SU[((size_t)2 * h + u) * XTS + e] = dlc;
+          SE[((size_t)0 * TT + e) * h + u] = sg;
+          SE[((size_t)1 * TT + e) * h + u] = dl;
+          SE[((size_t)2 * TT + e) * h + u] = dlc;
           DW[(size_t)e * h + u] = g * z + (-g) * zc;
         }
       }
@@ -776,18 +779,18 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
         const int sl = it / D2, j = it - sl * D2, ws = sl == n ? c : sl;
         const int cls = sl == c ? 1 : (sl == n ? 2 : 0);
         const float* wt = p.W1T + (size_t)ws * d + j;   // rows j and j + D2, + u * nd
-        const float4* su = reinterpret_cast<const float4*>(SU + (size_t)cls * h * kXTS);
-        float2 acc[2][kTT / 2];
+        const float4* su = reinterpret_cast<const float4*>(SU + (size_t)cls * h * XTS);
+        float2 acc[2][TT / 2];
 #pragma unroll
-        for (int q = 0; q < kTT / 2; ++q) acc[0][q] = acc[1][q] = make_float2(0.f, 0.f);
+        for (int q = 0; q < TT / 2; ++q) acc[0][q] = acc[1][q] = make_float2(0.f, 0.f);
         const int rot = (int)((blockIdx.x * 37u) % (unsigned)h);   // as in the forward
 #pragma unroll 16
         for (int uu = 0; uu < h; ++uu) {
           const int u = uu + rot < h ? uu + rot : uu + rot - h;
           const float w0 = __ldg(wt + (size_t)u * nd), w1 = __ldg(wt + (size_t)u * nd + D2);
 #pragma unroll
-          for (int q = 0; q < kTT / 4; ++q) {
-            const float4 sv = su[u * (kXTS / 4) + q];
+          for (int q = 0; q < TT / 4; ++q) {
+            const float4 sv = su[u * (XTS / 4) + q];
             const float2 lo = make_float2(sv.x, sv.y), hi = make_float2(sv.z, sv.w);
             acc[0][2 * q] = __ffma2_rn(lo, make_float2(w0, w0), acc[0][2 * q]);
             acc[0][2 * q + 1] = __ffma2_rn(hi, make_float2(w0, w0), acc[0][2 * q + 1]);
@@ -798,7 +801,7 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
 #pragma unroll
         for (int rr2 = 0; rr2 < 2; ++rr2)
 #pragma unroll
-          for (int q = 0; q < kTT / 2; ++q) {
+          for (int q = 0; q < TT / 2; ++q) {
             Gs[((size_t)(2 * q) * E + sl) * d + j + rr2 * D2] = acc[rr2][q].x;
             Gs[((size_t)(2 * q + 1) * E + sl) * d + j + rr2 * D2] = acc[rr2][q].y;
           }
@@ -817,7 +820,7 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
       const bool has_u = u0 < h;
       const int nA = n * d;
       int cur_cls = -1;
-      float2 sreg[kTT][2];
+      float2 sreg[TT][2];
       constexpr int LA = 4;   // record-row lookahead
       float4 pre[LA];
 #pragma unroll
@@ -834,17 +837,17 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
         if (cls != cur_cls) {
           cur_cls = cls;
 #pragma unroll
-          for (int e = 0; e < kTT; ++e) {
-            const float4 v = has_u ? *reinterpret_cast<const float4*>(SE + ((size_t)cls * kTT + e) * h + u0)
+          for (int e = 0; e < TT; ++e) {
+            const float4 v = has_u ? *reinterpret_cast<const float4*>(SE + ((size_t)cls * TT + e) * h + u0)
                                    : make_float4(0.f, 0.f, 0.f, 0.f);
             sreg[e][0] = make_float2(v.x, v.y);
             sreg[e][1] = make_float2(v.z, v.w);
           }
         }
-        const float4* xt4 = reinterpret_cast<const float4*>(XT + ((size_t)sl * d + j) * kXTS);
+        const float4* xt4 = reinterpret_cast<const float4*>(XT + ((size_t)sl * d + j) * XTS);
         float2 a0 = make_float2(0.f, 0.f), a1 = a0;
 #pragma unroll
-        for (int q = 0; q < kTT / 4; ++q) {
+        for (int q = 0; q < TT / 4; ++q) {
           const float4 x = xt4[q];
           const float xe[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -855,14 +858,14 @@ __device__ void phase1_tiled(const StepParams& p, unsigned char* sm) {
           }
         }
         if (cls == 1 && has_u) {   // centre block: + x'_c * delta'
-          const float4* xc4 = reinterpret_cast<const float4*>(XT + ((size_t)n * d + j) * kXTS);
+          const float4* xc4 = reinterpret_cast<const float4*>(XT + ((size_t)n * d + j) * XTS);
 #pragma unroll
-          for (int q = 0; q < kTT / 4; ++q) {
+          for (int q = 0; q < TT / 4; ++q) {
             const float4 x = xc4[q];
             const float xe[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-              const float4 v = *reinterpret_cast<const float4*>(SE + ((size_t)2 * kTT + 4 * q + t) * h + u0);
+              const float4 v = *reinterpret_cast<const float4*>(SE + ((size_t)2 * TT + 4 * q + t) * h + u0);
               const float2 xp = make_float2(xe[t], xe[t]);
               a0 = __ffma2_rn(make_float2(v.x, v.y), xp, a0);
               a1 = __ffma2_rn(make_float2(v.z, v.w), xp, a1);
@@ -1927,7 +1930,7 @@ __device__ void build_record(const StepParams& p, unsigned char* sm) {
 }
 
 // ------------------------------------------------------------------ kernels
-template <int PATH>   // 0 generic, 1 fast (h == 32), 2 tiled
+template <int PATH>   // 0 generic, 1 fast (h == 32), 2 tiled (16-example chunks), 3 tiled (4-example chunks)
 __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + p.lay.mbar);
@@ -1942,7 +1945,8 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
   trace_clock(p, 12);
   if (phases & 1) {
     if (PATH == 1) phase1_fast(p, smem);
-    else if (PATH == 2) phase1_tiled(p, smem);
+    else if (PATH == 2) phase1_tiled_t<kTT>(p, smem);
+    else if (PATH == 3) phase1_tiled_t<kTTSmall>(p, smem);
     else phase1_generic(p, smem);
     __syncthreads();
     trace_mark(p, 6);
@@ -1977,8 +1981,10 @@ int step_block_threads(int d, int n, int h, int fast) {
   return 384;
 }
 
-int step_chunk_T(int d, int n, int h, int fast) {
-  if (fast == 2) return kTT;
+int step_chunk_T(int d, int n, int h, int fast, int per_cta) {
+  // tiled path: a 4-example chunk when no CTA has more (the large config at
+  // 512 examples per GPU: 3.5 per CTA), else 16
+  if (fast == 2) return per_cta <= kTTSmall ? kTTSmall : kTT;
   int T = kTMax;
   while ((n + 1) * T > kMaxKeys) --T;
   if (!fast) {
@@ -1987,24 +1993,34 @@ int step_chunk_T(int d, int n, int h, int fast) {
   return T;
 }
 
-static const void* step_fn(int fast) {
-  return fast == 1 ? (const void*)step_kernel<1> : fast == 2 ? (const void*)step_kernel<2> : (const void*)step_kernel<0>;
+// The tiled path has one kernel per chunk size, so neither carries the other's
+// code (a combined kernel ran the 16-example case 12 % slower).
+static const void* step_fn(int fast, int T) {
+  if (fast == 2) return T == kTTSmall ? (const void*)step_kernel<3> : (const void*)step_kernel<2>;
+  return fast == 1 ? (const void*)step_kernel<1> : (const void*)step_kernel<0>;
 }
 
 // Allow up to the opt-in maximum minus the kernel's static shared memory.
 cudaError_t step_prepare(int fast, size_t optin, size_t* usable) {
-  const void* fn = step_fn(fast);
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
-  if (e != cudaSuccess) return e;
-  const size_t smem = optin - fa.sharedSizeBytes;
-  if (usable) *usable = smem;
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  size_t best = optin;
+  for (int T : {kTT, kTTSmall}) {
+    const void* fn = step_fn(fast, T);
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return e;
+    const size_t smem = optin - fa.sharedSizeBytes;
+    if (smem < best) best = smem;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (fast != 2) break;
+  }
+  if (usable) *usable = best;
+  return cudaSuccess;
 }
 
 void launch_step_phases(const StepParams& p, int phases, int fast, cudaStream_t s, int* launches) {
   const int NT = step_block_threads(p.d, p.n, p.h, fast);
-  const void* fn = step_fn(fast);
+  const void* fn = step_fn(fast, p.T);
   void* args[] = {(void*)&p, (void*)&phases};
   if ((phases & 1) && (phases & 6)) cudaLaunchCooperativeKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
   else cudaLaunchKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
@@ -2014,7 +2030,7 @@ void launch_step_phases(const StepParams& p, int phases, int fast, cudaStream_t 
 void launch_step(const StepParams& p, int fused, int fast, cudaStream_t s, int* launches) {
   const int NT = step_block_threads(p.d, p.n, p.h, fast);
   const size_t smem = (size_t)p.smem_bytes;
-  const void* fn = step_fn(fast);
+  const void* fn = step_fn(fast, p.T);
   if (fused) {
     int phases = 3;
     void* args[] = {(void*)&p, (void*)&phases};

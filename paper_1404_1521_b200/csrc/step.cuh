@@ -207,7 +207,7 @@ void launch_step(const StepParams& p, int fused, int fast, cudaStream_t s, int* 
 void launch_step_phases(const StepParams& p, int phases, int fast, cudaStream_t s, int* launches);
 int step_fast_ok(int d, int n, int h);
 int step_block_threads(int d, int n, int h, int fast);
-int step_chunk_T(int d, int n, int h, int fast);
+int step_chunk_T(int d, int n, int h, int fast, int per_cta);   // per_cta = ceil(B / P)
 cudaError_t step_prepare(int fast, size_t optin, size_t* usable);
 
 }  // namespace pg
