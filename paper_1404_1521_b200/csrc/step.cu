@@ -646,6 +646,7 @@ __device__ void phase1_fast(const StepParams& p, unsigned char* sm) {
 //              adds into this CTA's dense record (CTA-private, chunk order).
 constexpr int kTT = 16;   // chunk size of the tiled path (kTTSmall when every CTA has <= 4 examples)
 constexpr int kTTSmall = 4;
+constexpr int kTTMid = 8;
 template <int TT>
 __device__ void phase1_tiled_t(const StepParams& p, unsigned char* sm) {
   constexpr int XTS = TT + 4;   // XT row stride (floats): TT examples + 4 pad, 16 B aligned
@@ -1930,7 +1931,7 @@ __device__ void build_record(const StepParams& p, unsigned char* sm) {
 }
 
 // ------------------------------------------------------------------ kernels
-template <int PATH>   // 0 generic, 1 fast (h == 32), 2 tiled (16-example chunks), 3 tiled (4-example chunks)
+template <int PATH>   // 0 generic, 1 fast (h == 32), 2/3/4 tiled with 16/4/8-example chunks
 __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + p.lay.mbar);
@@ -1947,6 +1948,7 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
     if (PATH == 1) phase1_fast(p, smem);
     else if (PATH == 2) phase1_tiled_t<kTT>(p, smem);
     else if (PATH == 3) phase1_tiled_t<kTTSmall>(p, smem);
+    else if (PATH == 4) phase1_tiled_t<kTTMid>(p, smem);
     else phase1_generic(p, smem);
     __syncthreads();
     trace_mark(p, 6);
@@ -1982,9 +1984,9 @@ int step_block_threads(int d, int n, int h, int fast) {
 }
 
 int step_chunk_T(int d, int n, int h, int fast, int per_cta) {
-  // tiled path: a 4-example chunk when no CTA has more (the large config at
-  // 512 examples per GPU: 3.5 per CTA), else 16
-  if (fast == 2) return per_cta <= kTTSmall ? kTTSmall : kTT;
+  // tiled path: the smallest of 4 / 8 / 16-example chunks that holds a CTA's
+  // share (the large config at 512 examples per GPU: 3.5 per CTA)
+  if (fast == 2) return per_cta <= kTTSmall ? kTTSmall : per_cta <= kTTMid ? kTTMid : kTT;
   int T = kTMax;
   while ((n + 1) * T > kMaxKeys) --T;
   if (!fast) {
@@ -1996,14 +1998,15 @@ int step_chunk_T(int d, int n, int h, int fast, int per_cta) {
 // The tiled path has one kernel per chunk size, so neither carries the other's
 // code (a combined kernel ran the 16-example case 12 % slower).
 static const void* step_fn(int fast, int T) {
-  if (fast == 2) return T == kTTSmall ? (const void*)step_kernel<3> : (const void*)step_kernel<2>;
+  if (fast == 2)
+    return T == kTTSmall ? (const void*)step_kernel<3> : T == kTTMid ? (const void*)step_kernel<4> : (const void*)step_kernel<2>;
   return fast == 1 ? (const void*)step_kernel<1> : (const void*)step_kernel<0>;
 }
 
 // Allow up to the opt-in maximum minus the kernel's static shared memory.
 cudaError_t step_prepare(int fast, size_t optin, size_t* usable) {
   size_t best = optin;
-  for (int T : {kTT, kTTSmall}) {
+  for (int T : {kTT, kTTSmall, kTTMid}) {
     const void* fn = step_fn(fast, T);
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, fn);

@@ -26,7 +26,7 @@ def pg():
 
 
 @pytest.mark.parametrize("cfg", SHAPES, ids=lambda c: f"d{c['d']}n{c['n']}h{c['h']}")
-@pytest.mark.parametrize("B", [5, 300, 2400 + 13])
+@pytest.mark.parametrize("B", [5, 300, 1000, 2400 + 13])   # 4-, 4-, 8- and 16-example chunks
 def test_tiled_parity(pg, cfg, B):
     # B = 2413 > 148 * 16: several 16-example chunks per CTA (record RMW path)
     m = pg.PolyglotModel(cfg["V"], cfg["d"], cfg["n"], cfg["h"], seed=11)
