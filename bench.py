@@ -350,6 +350,32 @@ def main():
         dist.destroy_process_group()
 
 
+def oracle_timings(np, synth):
+    """The float64 oracle as it stands (1 host thread) on the other configs of
+    SURVEY.md 8(d): tiny, large (one step, batch 512), and the serial
+    index_add of the 1M-row scatter microbench in fp64 and fp32."""
+    import oracle
+    out = {}
+    for name, (V, d, n, h, B, steps) in {"tiny_v1k_d16_n5_h32_b16": (1000, 16, 5, 32, 16, 100),
+                                         "large_v1m_d128_n5_h128_b512": (1_000_000, 128, 5, 128, 512, 1)}.items():
+        p = oracle.Params.init(V, d, n, h, 42)
+        bs = [synth.batch(V, n, B, seed=42, step=t) for t in range(steps)]
+        t0 = time.perf_counter()
+        for idx, corr in bs:
+            oracle.train_step(p, idx, corr, 0.1)
+        dt = time.perf_counter() - t0
+        out[name] = {"examples_per_s": B * steps / dt, "steps": steps}
+    I, Y = synth.scatter_inputs(100_000, 64, 1_000_000, "zipf", "random", seed=42)
+    for dt_name, dtype in (("f64", np.float64), ("f32", np.float32)):
+        W = np.zeros((100_000, 64), dtype)
+        Yc = Y.astype(dtype)
+        t0 = time.perf_counter()
+        oracle.index_add(W, Yc, I)
+        out[f"index_add_1M_zipf_{dt_name}_s"] = time.perf_counter() - t0
+    out["cores"] = 1
+    return out
+
+
 def run_extras(pg, torch, synth, np, dev, stream, flush, model):
     """Batch sweep (configs[1]) and the scatter-add microbench (configs[2])."""
     V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
@@ -456,6 +482,7 @@ def run_extras(pg, torch, synth, np, dev, stream, flush, model):
     big.close()
     res["large_config"] = {"config": "V 1M, d 128, n 5, h 128 (BASELINE.json configs[3] shape), L2 flushed, 1 GPU",
                            "path": "tiled phase 1 (FFMA2)", "results": lg}
+    res["oracle_timings"] = oracle_timings(np, synth)
     return res
 
 
