@@ -400,7 +400,12 @@ def run_extras(pg, torch, synth, np, dev, stream, flush, model):
                 tms.append((a, b))
             torch.cuda.synchronize()
         ms = [a.elapsed_time(b) for a, b in tms]
-        sweep[str(B)] = {"us_per_step": 1e3 * statistics.mean(ms), "examples_per_s": B / (statistics.mean(ms) / 1e3)}
+        # distinct embedding rows a step touches (read once, written once): the
+        # table traffic the step cannot avoid, as GB/s of the step time
+        uniq = statistics.mean(len(np.unique(np.concatenate([i.ravel(), c]))) for i, c in bs)
+        sweep[str(B)] = {"us_per_step": 1e3 * statistics.mean(ms), "examples_per_s": B / (statistics.mean(ms) / 1e3),
+                         "unique_rows": uniq,
+                         "unique_row_gbs": uniq * 2 * 4 * d / (statistics.mean(ms) / 1e3) / 1e9}
     model.sync()
     res["batch_sweep_l2_flushed"] = sweep
     # the paper's own operating point (B = 16), as context only: GT 570 + Theano
