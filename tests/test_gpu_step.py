@@ -253,3 +253,37 @@ def test_async_host_inputs_pipeline_equals_device_inputs(pg):
     for x, y in zip(a.get_params()[:4], b.get_params()[:4]):
         assert np.array_equal(x, y)
     a.close(); b.close()
+
+
+def test_cuda_graph_capture_replay_equals_eager(pg):
+    """PG_OPT_RESERVE pre-sizes the workspace so steps with device inputs and a
+    device loss can be captured in a CUDA graph; replaying the graph must give
+    the same (DET: bitwise) parameters and losses as eager calls."""
+    import torch
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    B, K = 2048, 3
+    bs = [synth.batch(V, n, B, seed=21, step=t) for t in range(K)]
+    di = [torch.from_numpy(i).cuda() for i, _ in bs]
+    dc = [torch.from_numpy(c).cuda() for _, c in bs]
+    s = torch.cuda.Stream()
+    eager = pg.PolyglotModel(V, d, n, h, seed=5, stream=s)
+    graphed = pg.PolyglotModel(V, d, n, h, seed=5, stream=s)
+    graphed.reserve(B)
+    le = torch.zeros(K, device="cuda")
+    lg = torch.zeros(K, device="cuda")
+    with torch.cuda.stream(s):
+        for t in range(K):
+            eager.train_step(di[t], dc[t], 0.1, loss_out=le[t:t + 1])
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for t in range(K):
+            graphed.train_step(di[t], dc[t], 0.1, loss_out=lg[t:t + 1])
+    # capture records the launches without running them: the parameters are
+    # still the initial ones until the replay
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(le, lg)
+    for a, b in zip(eager.get_params(), graphed.get_params()):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+    eager.close(); graphed.close()
