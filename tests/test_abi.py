@@ -59,3 +59,26 @@ def test_product_package_does_not_import_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower() or f == "__init__.py" and \
                     "import oracle" not in txt, f
+
+
+def test_header_constants_match_binding():
+    """Every PG_* enumerator in pg.h has the same value in the Python binding."""
+    import paper_1404_1521_b200 as pg
+    src = open(os.path.join(ROOT, "include", "pg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    consts = {}
+    for body in re.findall(r"enum\s*\w*\s*\{(.*?)\}", src, flags=re.S):
+        nxt = 0
+        for item in [x.strip() for x in body.split(",") if x.strip()]:
+            m = re.match(r"(PG_\w+)\s*(?:=\s*(-?\d+))?$", item)
+            assert m, item
+            val = int(m.group(2)) if m.group(2) is not None else nxt
+            consts[m.group(1)] = val
+            nxt = val + 1
+    for name in ("PG_OK", "PG_ERANGE", "PG_EDIVERGED", "PG_SCATTER_DET", "PG_SCATTER_ATOMIC", "PG_OPT_SCATTER",
+                 "PG_OPT_RESERVE", "PG_OPT_ACTIVATION", "PG_OPT_REDUCTION", "PG_ACT_HARDTANH", "PG_ACT_TANH",
+                 "PG_REDUCE_MEAN", "PG_REDUCE_SUM"):
+        assert name in consts, name
+    for name, val in consts.items():
+        if hasattr(pg, name):
+            assert getattr(pg, name) == val, (name, getattr(pg, name), val)
