@@ -638,18 +638,18 @@ __global__ void sc_validate(const int32_t* __restrict__ I, int64_t n, int64_t ro
 //     kHotSample entries in an smem hash: rows seen >= kHotMin times
 //     (relative frequency >~ 0.1 %) are ranked by (count desc, row asc) with a
 //     bitonic sort, so every CTA derives the same ranking -- the first ha go to
-//     tier A (a private smem accumulator per warp), the next up to kHotB to
+//     tier A (a private smem accumulator per lane group), the next up to kHotB to
 //     tier B (kHotRep replica rows each, in global memory);
 //  2. barrier wait (a bad index anywhere means nothing is applied);
 //  3. warps take batches of 32 consecutive entries, interleaved over the
 //     grid: lane i loads I[b0 + i] and probes the hot set for it, then the
 //     lane groups stream the batch's Y rows (evict-first loads, U rows in
 //     flight per lane group; row and slot arrive by shuffles): a tier-A row
-//     is added into the warp's private accumulator (the warp's lane groups
-//     take turns, no atomics), a tier-B row goes by red.global.add.v4.f32 to
+//     is added into its lane group's private accumulator (a plain
+//     read-modify-write, no atomics), a tier-B row goes by red.global.add.v4.f32 to
 //     one of its replica rows (by entry position: 1/kHotRep of the per-line
 //     serialisation), every other row straight to W the same way;
-//  4. tier A (summed over warps in warp order) reaches W with one vector
+//  4. tier A (summed over the copies in order) reaches W with one vector
 //     reduction per 16 B per CTA; after a second grid barrier, CTA c folds the
 //     replica rows of tier-B rows c, c + grid, ... into W and zeroes them for
 //     the next call.
@@ -782,9 +782,10 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   const int na = nh < ha ? nh : ha, nb = nh - na;
   __syncthreads();
   // tier A: [NW][na][q] private copies (dense for the rows actually taken)
-  for (int t = tid; t < NW * na * q; t += kThreads)
+  const int NC = NW * per;   // tier-A copies: one per lane group (no turn-taking)
+  for (int t = tid; t < NC * na * q; t += kThreads)
     reinterpret_cast<float4*>(accA)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4* accw = reinterpret_cast<float4*>(accA) + (size_t)warp * na * q;
+  float4* accw = reinterpret_cast<float4*>(accA) + (size_t)(warp * per + (sub < per ? sub : 0)) * na * q;
   const bool act = sub < per && gl < q;
   // Warp batches of 32 consecutive entries: lane i loads I[b0 + i] and probes
   // the hot set once for it; the lane groups then take the batch's entries
@@ -829,17 +830,11 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
         if (row[u] >= 0 && sv < 0) red_add_v4(W + (row[u] * cols + 4 * gl), v[u]);
         if (sv >= na)   // tier B: one of kHotRep replica rows, by entry position
           red_add_v4(rep + ((sv - na) * kHotRep + (k0 + u * per + sub) % kHotRep) * cols + 4 * gl, v[u]);
-        const bool isA = sv >= 0 && sv < na;
-        if (__any_sync(0xffffffffu, isA)) {
-          for (int hs = 0; hs < per; ++hs) {
-            if (sub == hs && isA) {
-              float4* p = accw + sv * q + gl;
-              float4 t = *p;
-              t.x += v[u].x; t.y += v[u].y; t.z += v[u].z; t.w += v[u].w;
-              *p = t;
-            }
-            __syncwarp();
-          }
+        if (sv >= 0 && sv < na) {   // this lane group's own copy: a plain read-modify-write
+          float4* p = accw + sv * q + gl;
+          float4 t = *p;
+          t.x += v[u].x; t.y += v[u].y; t.z += v[u].z; t.w += v[u].w;
+          *p = t;
         }
       }
     }
@@ -850,7 +845,7 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     const int r = t / q, f = t - r * q;
     const float4* a = reinterpret_cast<const float4*>(accA) + (size_t)r * q + f;
     float4 sm4 = a[0];
-    for (int w = 1; w < NW; ++w) {
+    for (int w = 1; w < NC; ++w) {
       const float4 b = a[(size_t)w * na * q];
       sm4.x += b.x; sm4.y += b.y; sm4.z += b.z; sm4.w += b.w;
     }
@@ -921,14 +916,18 @@ static const void* const kHotFn = (const void*)sc_atomic_hot<kHotThreads, 4>;
 constexpr size_t kHotSmemMax = 200 * 1024;
 // tier-A rows per warp and tier-B rows for a row width: tier A gets up to 32
 // rows if the warps' copies fit in 2/3 of the budget, tier B the rest (<= kHotB).
+static int hot_copies(int cols) {   // tier-A copies per CTA: one per lane group of cols/4 lanes
+  const int q = cols / 4, G = q >= 32 ? 32 : q;
+  return (kHotThreads / 32) * (32 / G);
+}
 static void hot_tiers(int cols, int* ha, int* hb) {
-  const size_t row = sizeof(float) * cols, nw = kHotThreads / 32;
-  int a = (int)(kHotSmemMax / (nw * row));
+  const size_t row = sizeof(float) * cols;
+  int a = (int)(kHotSmemMax / ((size_t)hot_copies(cols) * row));
   *ha = a > 32 ? 32 : a;
   *hb = kHotB;   // tier B lives in global replica rows (ScatterPlan::off_rep)
 }
 static size_t hot_smem(int ha, int cols) {
-  const size_t acc = sizeof(float) * (size_t)(kHotThreads / 32) * ha * cols;
+  const size_t acc = sizeof(float) * (size_t)hot_copies(cols) * ha * cols;
   const size_t samp = sizeof(int) * 2 * kHotSampleHash + sizeof(unsigned long long) * kHotCand;
   return acc > samp ? acc : samp;
 }
