@@ -661,7 +661,7 @@ constexpr int kHotHash = 1024;
 constexpr int kHotB = 256;
 constexpr int kHotMin = 4;                          // sample count of a hot row
 constexpr int kHotCand = kHotSample / kHotMin;      // 1024: every row seen >= kHotMin times
-constexpr int kHotRep = 8;                          // replica rows per tier-B row
+constexpr int kHotRep = 16;                         // replica rows per tier-B row
 constexpr size_t kHotPrefetchMax = 48u << 20;
 template <int kThreads, int U>
 __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __restrict__ I,
@@ -914,8 +914,7 @@ __global__ void sc_atomic_scalar(const int32_t* __restrict__ I, const float* __r
 constexpr int kHotThreads = 1024;
 static const void* const kHotFn = (const void*)sc_atomic_hot<kHotThreads, 4>;
 constexpr size_t kHotSmemMax = 200 * 1024;
-// tier-A rows per warp and tier-B rows for a row width: tier A gets up to 32
-// rows if the warps' copies fit in 2/3 of the budget, tier B the rest (<= kHotB).
+// tier-A rows (one copy per lane group) and tier-B rows for a row width.
 static int hot_copies(int cols) {   // tier-A copies per CTA: one per lane group of cols/4 lanes
   const int q = cols / 4, G = q >= 32 ? 32 : q;
   return (kHotThreads / 32) * (32 / G);
@@ -923,7 +922,11 @@ static int hot_copies(int cols) {   // tier-A copies per CTA: one per lane group
 static void hot_tiers(int cols, int* ha, int* hb) {
   const size_t row = sizeof(float) * cols;
   int a = (int)(kHotSmemMax / ((size_t)hot_copies(cols) * row));
-  *ha = a > 32 ? 32 : a;
+  // at most 8 tier-A rows: the copies' shared memory shrinks the L1, which the
+  // uniform case pays for (12 rows: 85.4 us, 8: 77.9 us L2-flushed) while the
+  // Zipf case is no faster with more (88.1 us either way, scripts/ab_atomic.sh)
+  *ha = a > 8 ? 8 : a;
+  (void)a;
   *hb = kHotB;   // tier B lives in global replica rows (ScatterPlan::off_rep)
 }
 static size_t hot_smem(int ha, int cols) {
