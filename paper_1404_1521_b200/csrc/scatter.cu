@@ -761,16 +761,20 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   while (npow < nc) npow <<= 1;
   for (int i = nc + tid; i < npow; i += kThreads) cand[i] = ~0ull;
   __syncthreads();
-  for (int size = 2; size <= npow; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = tid; t < npow / 2; t += kThreads) {
-        const int lo2 = 2 * t - (t & (stride - 1)), hi2 = lo2 + stride;
-        const bool up = (lo2 & size) == 0;
-        const unsigned long long x = cand[lo2], y = cand[hi2];
-        if ((x > y) == up) { cand[lo2] = y; cand[hi2] = x; }
+  if (npow >= 32) {
+    bitonic_sort_warp(cand, npow);   // strides < 32 in registers (common.cuh)
+  } else {
+    for (int size = 2; size <= npow; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = tid; t < npow / 2; t += kThreads) {
+          const int lo2 = 2 * t - (t & (stride - 1)), hi2 = lo2 + stride;
+          const bool up = (lo2 & size) == 0;
+          const unsigned long long x = cand[lo2], y = cand[hi2];
+          if ((x > y) == up) { cand[lo2] = y; cand[hi2] = x; }
+        }
+        __syncthreads();
       }
-      __syncthreads();
-    }
+  }
   const int nh = nc < ha + hb ? nc : ha + hb;
   for (int a = tid; a < nh; a += kThreads) {
     const int r = (int)(unsigned)(cand[a] & 0xffffffffull);

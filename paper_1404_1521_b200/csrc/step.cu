@@ -1193,60 +1193,6 @@ __device__ __forceinline__ void fb_segsum(float* stage, float* carry, int d, int
   }
 }
 
-// Bitonic sort of n (power of two, >= 32) 64-bit keys in smem with the
-// sub-steps of stride < 32 done in registers by warp shuffles: key i sits at
-// lane i % 32 of group i / 32, warp w takes groups w, w + #warps, ...  Only the
-// stride >= 32 sub-steps go through shared memory, so a 1024-key sort needs 21
-// block barriers instead of 55.  Same network, same result as bitonic_sort.
-__device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v, int m) {
-  const unsigned lo = __shfl_xor_sync(0xffffffffu, (unsigned)v, m);
-  const unsigned hi = __shfl_xor_sync(0xffffffffu, (unsigned)(v >> 32), m);
-  return ((unsigned long long)hi << 32) | lo;
-}
-__device__ void bitonic_sort_warp(unsigned long long* k, int n) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5, G = n >> 5;
-  // sub-steps with stride in [1, top] of stage `size`, for every group of this warp
-  auto warp_steps = [&](int size, int top) {
-    for (int g = warp; g < G; g += NW) {
-      const int i = g * 32 + lane;
-      unsigned long long v = k[i];
-      for (int stride = top; stride > 0; stride >>= 1) {
-        const unsigned long long o = shfl_xor_u64(v, stride);
-        const bool up = (i & size) == 0, lower = (lane & stride) == 0;
-        const bool take_min = lower == up;
-        v = take_min ? (o < v ? o : v) : (o > v ? o : v);
-      }
-      k[i] = v;
-    }
-  };
-  for (int g = warp; g < G; g += NW) {   // stages of size 2..32 entirely in registers
-    const int i = g * 32 + lane;
-    unsigned long long v = k[i];
-    for (int sz = 2; sz <= 32; sz <<= 1)
-      for (int stride = sz >> 1; stride > 0; stride >>= 1) {
-        const unsigned long long o = shfl_xor_u64(v, stride);
-        const bool up = (i & sz) == 0, lower = (lane & stride) == 0;
-        v = (lower == up) ? (o < v ? o : v) : (o > v ? o : v);
-      }
-    k[i] = v;
-  }
-  __syncthreads();
-  for (int size = 64; size <= n; size <<= 1) {
-    for (int stride = size >> 1; stride >= 32; stride >>= 1) {
-      for (int t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
-        const int lo = 2 * t - (t & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const unsigned long long a = k[lo], b = k[hi];
-        if ((a > b) == up) { k[lo] = b; k[hi] = a; }
-      }
-      __syncthreads();
-    }
-    warp_steps(size, 16);
-    __syncthreads();
-  }
-}
-
 // Sorted fallback for owners with more than MCAP entries (pathological index
 // patterns): windows of whole lists, bitonic sort by (row, list), segment sums
 // in list order with a carry across staged sub-batches.
