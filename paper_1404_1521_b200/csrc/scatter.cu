@@ -660,7 +660,8 @@ constexpr int kHotSampleHash = 8192;
 constexpr int kHotHash = 1024;
 constexpr int kHotB = 256;
 constexpr int kHotMin = 4;                          // sample count of a hot row
-constexpr int kHotCand = kHotSample / kHotMin;      // 1024: every row seen >= kHotMin times
+constexpr int kHotCand = 1024;   // power of two >= kHotSample / kHotMin: every row seen >= kHotMin times
+static_assert((kHotCand & (kHotCand - 1)) == 0 && kHotCand >= kHotSample / kHotMin, "candidate array");
 constexpr int kHotRep = 16;                         // replica rows per tier-B row
 constexpr size_t kHotPrefetchMax = 48u << 20;
 template <int kThreads, int U>
@@ -680,13 +681,17 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   const int q = cols >> 2;
   const int G = q >= 32 ? 32 : q, per = 32 / G, sub = lane / G, gl = lane % G;
   const int64_t ns = n < kHotSample ? n : kHotSample;
-  const int64_t sstride = n / (ns > 0 ? ns : 1);
+  // the sample: ns / 32 runs of 32 consecutive entries spread evenly over I
+  // (one 128 B line per warp load: every CTA reads the same lines, so
+  // per-entry strided sampling put 148 x 4096 sector requests on the L2)
+  const int64_t nruns = (ns + 31) / 32;
+  const int64_t rstride = n / (nruns > 0 ? nruns : 1);
   constexpr int kSPer = (kHotSample + kThreads - 1) / kThreads;
   int samp[kSPer];
 #pragma unroll
   for (int j = 0; j < kSPer; ++j) {
     const int64_t i = (int64_t)j * kThreads + tid;
-    samp[j] = i < ns ? __ldg(I + i * sstride) : -1;
+    samp[j] = i < ns ? __ldg(I + (n <= kHotSample ? i : (i >> 5) * rstride + (i & 31))) : -1;
   }
   {   // validation: this CTA's grid-strided share, 4 x int4 per thread per trip
     const int64_t n4 = ((uintptr_t)I & 15) == 0 ? n >> 2 : 0;
