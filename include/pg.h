@@ -161,7 +161,7 @@ pg_status pg_sync(pg_model* m);
  * k order within fixed-size chunks, chunk partials combined in chunk order:
  * bit-reproducible run to run (cols in {1..32, 64, 128}).  mode
  * PG_SCATTER_ATOMIC: one streaming pass over Y; the rows that a fixed
- * strided sample of I shows to be frequent (>~0.1 % of entries) are summed in
+ * spread sample of I shows to be frequent (>~0.1 % of entries) are summed in
  * shared memory per CTA (the most frequent) or spread over replica rows in the
  * library's workspace, every other entry reaches W through
  * red.global.add.v4.f32 per 16 B (cols % 4 == 0, cols <= 128; other widths

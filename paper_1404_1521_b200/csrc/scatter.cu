@@ -634,7 +634,7 @@ __global__ void sc_validate(const int32_t* __restrict__ I, int64_t n, int64_t ro
 //  1. every CTA checks its grid-strided share of I (all loads issued at once)
 //     and arrives at the grid barrier; while the barrier completes it
 //     prefetches its share of W into L2 (when W is small next to the L2) and,
-//     redundantly and identically, counts a fixed strided sample of
+//     redundantly and identically, counts a fixed sample (128 evenly spread runs of 32 entries) of
 //     kHotSample entries in an smem hash: rows seen >= kHotMin times
 //     (relative frequency >~ 0.1 %) are ranked by (count desc, row asc) with a
 //     bitonic sort, so every CTA derives the same ranking -- the first ha go to
