@@ -15,15 +15,22 @@ Parity pins for every function (none is "parity unpinned"):
     gradient, saturation / inactive-hinge special cases;
   * pgo_index_add(_f32)      -- SPEC.md:67-69 worked examples, the
     10000-ones example (SPEC.md:130), decomposability (SPEC.md:81-84);
-  * pgo_train_step(_dp)      -- zero-params fixed point, b2 invariance,
-    locality (SPEC.md:244), DP emulation == single step up to rounding;
+  * pgo_sgd_update           -- SPEC.md:237-238 worked examples (zero
+    gradients -> unchanged; lr=1 and one sparse row -> that embedding row
+    decreased by exactly the row), exact dyadic dense examples;
+  * pgo_train_step(_dp)      -- theta_new == theta - lr * g with g from
+    central finite differences of the loss (not pgo_backward), zero-params
+    fixed point, b2 invariance, locality, DP emulation ==
+    single step up to rounding;
   * tanh variant (pgo_set_activation(1)) -- finite differences (smooth, no
     kinks), the h=1 closed form s = tanh(c), zero-params fixed point;
   * sum reduction (pgo_set_reduction(1)) -- exact identities with the mean
     form (loss x B; one step at lr equals the mean step at lr x B for
     power-of-two B) and finite differences of the summed loss;
-  * pgo_init_params          -- golden hash under tests/golden/ written by a
-    script that calls only this package, plus range/moment checks.
+  * pgo_init_params          -- the init spec recomputed element by element
+    with the independently written numpy SplitMix64 of synth/ (itself pinned
+    to published SplitMix64 vectors, tests/golden/splitmix64_vectors.json),
+    plus range/moment checks.
 See tests/test_oracle_*.py.
 """
 from __future__ import annotations
@@ -120,6 +127,8 @@ def lib():
                                      i64, ctypes.c_double, P]
         L.pgo_train_step_dp.argtypes = [i64, i32, i32, i32, P, P, P, P, P, P, P,
                                         i64, i32, ctypes.c_double, P]
+        L.pgo_sgd_update.argtypes = [i64, i32, i32, i32, P, P, P, P, P, ctypes.c_double,
+                                     P, P, P, ctypes.c_double, P, P, i64]
         L.pgo_index_add.argtypes = [P, i64, i32, P, P, i64]
         L.pgo_index_add_f32.argtypes = [P, i64, i32, P, P, i64]
         L.pgo_last_bad.argtypes = [P, P]
@@ -128,7 +137,7 @@ def lib():
         L.pgo_set_reduction.argtypes = [i32]
         L.pgo_set_reduction.restype = ctypes.c_int
         for f in ("pgo_init_params", "pgo_forward", "pgo_backward", "pgo_score",
-                  "pgo_train_step", "pgo_train_step_dp", "pgo_index_add",
+                  "pgo_train_step", "pgo_train_step_dp", "pgo_index_add", "pgo_sgd_update",
                   "pgo_index_add_f32"):
             getattr(L, f).restype = ctypes.c_int
         L.pgo_last_bad.restype = None
@@ -227,6 +236,22 @@ def score(p: Params, idx):
     out = np.zeros(B)
     _check(lib().pgo_score(*p._args(), _p(idx), B, _p(out)), "pgo_score")
     return out
+
+
+def sgd_update(p: Params, grads: dict, lr) -> None:
+    """In-place SPEC.md:231-235 update: dense theta -= lr * grad, C by the serial
+    index_add of -lr * Y over grads["rows"]."""
+    h, nd = p.h, p.n * p.d
+    dW1 = np.ascontiguousarray(grads.get("dW1", np.zeros((nd, h))), np.float64)
+    db1 = np.ascontiguousarray(grads.get("db1", np.zeros(h)), np.float64)
+    dw2 = np.ascontiguousarray(grads.get("dw2", np.zeros(h)), np.float64)
+    rows = _i32(grads.get("rows", np.zeros(0, np.int32)))
+    Y = np.ascontiguousarray(grads.get("Y", np.zeros((0, p.d))), np.float64).reshape(-1, p.d)
+    if Y.shape[0] != rows.shape[0]:
+        raise ValueError("Y and rows disagree")
+    _check(lib().pgo_sgd_update(*p._args(), float(lr), _p(dW1), _p(db1), _p(dw2),
+                                float(grads.get("db2", 0.0)), _p(rows), _p(Y), rows.shape[0]),
+           "pgo_sgd_update")
 
 
 def train_step(p: Params, idx, corr, lr) -> float:

@@ -306,17 +306,26 @@ int pgo_index_add_f32(float* W, int64_t rows, int cols, const float* Y,
 }
 
 /* ---------------------------------------------------------------------- */
-/* One SGD step (SPEC.md:231-239; reading G8: every gradient and the       */
-/* returned loss use the pre-step parameters, then all updates apply):     */
-/*   theta -= lr * grad for W1, b1, w2, b2;                                 */
-/*   C: serial index_add of (-lr * Y) over the 2nB rows in emission order.  */
-/* A non-finite loss leaves every parameter unchanged (SPEC.md:313).        */
+/* sgd_update ("[OP] sgd_update ... post: dense params       */
+/* updated as theta -= lr * grad theta; embedding table updated via          */
+/* index_add(C, -lr * values, indices)"):                                    */
+/*   theta -= lr * grad for W1, b1, w2, b2;                                  */
+/*   C: serial index_add of (-lr * Y) over the rows in emission order.       */
+/* lr > 0 ("pre: lr > 0"); an out-of-range row leaves every      */
+/* parameter unchanged (checked before anything is written).                 */
 /* ---------------------------------------------------------------------- */
-static int apply_update(int64_t V, int d, int n, int h, double* C, double* W1,
-                        double* b1, double* w2, double* b2, double lr,
-                        const double* dW1, const double* db1, const double* dw2,
-                        double db2, const int32_t* rows, const double* Y,
-                        int64_t nrows) {
+int pgo_sgd_update(int64_t V, int d, int n, int h, double* C, double* W1,
+                   double* b1, double* w2, double* b2, double lr,
+                   const double* dW1, const double* db1, const double* dw2,
+                   double db2, const int32_t* rows, const double* Y,
+                   int64_t nrows) {
+  if (check_shape(V, d, n, h) || nrows < 0 || !(lr > 0.0) || !isfinite(lr))
+    return PGO_EINVAL;
+  for (int64_t k = 0; k < nrows; ++k)
+    if (rows[k] < 0 || rows[k] >= V) {
+      g_bad_pos = k; g_bad_val = rows[k];
+      return PGO_ERANGE;
+    }
   for (int64_t i = 0; i < (int64_t)n * d * h; ++i) W1[i] -= lr * dW1[i];
   for (int u = 0; u < h; ++u) {
     b1[u] -= lr * db1[u];
@@ -330,6 +339,11 @@ static int apply_update(int64_t V, int d, int n, int h, double* C, double* W1,
   return rc;
 }
 
+/* ---------------------------------------------------------------------- */
+/* One SGD step (SPEC.md:231-239; reading G8: every gradient and the       */
+/* returned loss use the pre-step parameters, then all updates apply).     */
+/* A non-finite loss leaves every parameter unchanged (SPEC.md:313).        */
+/* ---------------------------------------------------------------------- */
 int pgo_train_step(int64_t V, int d, int n, int h, double* C, double* W1,
                    double* b1, double* w2, double* b2, const int32_t* idx,
                    const int32_t* corr, int64_t B, double lr,
@@ -355,7 +369,7 @@ int pgo_train_step(int64_t V, int d, int n, int h, double* C, double* W1,
   rc = pgo_backward(V, d, n, h, C, W1, b1, w2, b2, idx, corr, B,
                     batch_scale(B), dW1, db1, dw2, &db2, rows, Y, &nrows);
   if (!rc)
-    rc = apply_update(V, d, n, h, C, W1, b1, w2, b2, lr, dW1, db1, dw2, db2,
+    rc = pgo_sgd_update(V, d, n, h, C, W1, b1, w2, b2, lr, dW1, db1, dw2, db2,
                       rows, Y, nrows);
   free(dW1); free(db1); free(dw2); free(rows); free(Y);
   return rc;
@@ -408,7 +422,7 @@ int pgo_train_step_dp(int64_t V, int d, int n, int h, double* C, double* W1,
     for (int u = 0; u < h; ++u) { db1[u] += gb1[u]; dw2[u] += gw2[u]; }
     db2 += gb2;
   }
-  rc = apply_update(V, d, n, h, C, W1, b1, w2, b2, lr, dW1, db1, dw2, db2,
+  rc = pgo_sgd_update(V, d, n, h, C, W1, b1, w2, b2, lr, dW1, db1, dw2, db2,
                     rows, Y, nrows);
   free(dW1); free(db1); free(dw2); free(gW1); free(gb1); free(gw2);
   free(rows); free(Y);

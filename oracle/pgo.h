@@ -61,6 +61,13 @@ int pgo_score(int64_t V, int d, int n, int h,
               const double* w2, const double* b2,
               const int32_t* idx, int64_t B, double* scores);
 
+/* theta -= lr * grad (dense), C via serial index_add of -lr * Y. */
+int pgo_sgd_update(int64_t V, int d, int n, int h,
+                   double* C, double* W1, double* b1, double* w2, double* b2,
+                   double lr, const double* dW1, const double* db1,
+                   const double* dw2, double db2,
+                   const int32_t* rows, const double* Y, int64_t nrows);
+
 int pgo_train_step(int64_t V, int d, int n, int h,
                    double* C, double* W1, double* b1, double* w2, double* b2,
                    const int32_t* idx, const int32_t* corr, int64_t B,

@@ -451,3 +451,94 @@ def test_sum_reduction_dp_emulation():
         lb = oracle.train_step_dp(b, idx, corr, 0.01, world=4)
     assert abs(la - lb) <= 1e-12 * abs(la)
     np.testing.assert_allclose(b.flat(), a.flat(), rtol=1e-13, atol=1e-16)
+
+
+# ---------------------------------------------------------------- update rule
+def test_sgd_update_spec_examples():
+    ex0, ex1 = _gold("spec_examples.json")["sgd_update"]
+    # zero gradients -> every parameter unchanged
+    V, d, n, h = 9, 3, 5, 4
+    p = oracle.Params.init(V, d, n, h, 3)
+    p.b2[0] = 0.25
+    q = p.copy()
+    oracle.sgd_update(q, {"rows": np.array(ex0["rows"], np.int32), "Y": np.zeros((0, d))}, ex0["lr"])
+    np.testing.assert_array_equal(q.flat(), p.flat(), err_msg=ex0["cite"])
+    # lr = 1, one sparse row -> that embedding row decreased by exactly the row
+    C = np.array(ex1["C"])
+    p = oracle.Params(C.shape[0], C.shape[1], 1, 1, C=C)
+    oracle.sgd_update(p, {"rows": np.array(ex1["rows"], np.int32), "Y": np.array(ex1["Y"])}, ex1["lr"])
+    np.testing.assert_array_equal(p.C, np.array(ex1["expect_C"]), err_msg=ex1["cite"])
+
+
+def test_sgd_update_dense_direction_and_scale():
+    # SPEC.md:234 "theta -= lr * grad": with lr = 0.5 and gradients 2 * e_i the
+    # parameter moves by exactly -1 (dyadic, exact in fp64) -- a sign or scale
+    # error in any dense tensor moves it the wrong way.
+    V, d, n, h = 4, 2, 3, 2
+    p = oracle.Params(V, d, n, h)
+    g = {"dW1": np.zeros((n * d, h)), "db1": np.zeros(h), "dw2": np.zeros(h), "db2": 0.0}
+    g["dW1"][4, 1] = 2.0; g["db1"][0] = 2.0; g["dw2"][1] = 2.0
+    oracle.sgd_update(p, g, 0.5)
+    assert p.W1[4, 1] == -1.0 and p.b1[0] == -1.0 and p.w2[1] == -1.0
+    assert np.count_nonzero(p.flat()) == 3
+    # duplicated sparse rows accumulate: two rows of +1 at lr 0.25 -> -0.5
+    oracle.sgd_update(p, {"rows": np.array([2, 2], np.int32), "Y": np.ones((2, d))}, 0.25)
+    np.testing.assert_array_equal(p.C[2], [-0.5, -0.5])
+    assert not p.C[[0, 1, 3]].any()
+
+
+def test_sgd_update_bad_row_no_mutation():
+    p = oracle.Params.init(6, 2, 3, 2, 1)
+    q = p.copy()
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.sgd_update(q, {"dW1": np.ones((6, 2)), "rows": np.array([1, 6], np.int32),
+                              "Y": np.ones((2, 2))}, 0.1)
+    assert e.value.status == 2
+    np.testing.assert_array_equal(q.flat(), p.flat())
+
+
+def _fd_grad(p, idx, corr):
+    """Central finite differences of the loss for every parameter (no pgo_backward)."""
+    out = []
+    for arr in (p.C, p.W1, p.b1, p.w2):
+        flat = arr.reshape(-1)
+        g = np.empty(flat.size)
+        for i in range(flat.size):
+            t = flat[i]
+            hs = 1e-6 * max(1.0, abs(t))
+            flat[i] = t + hs; lp = oracle.loss(p, idx, corr)
+            flat[i] = t - hs; lm = oracle.loss(p, idx, corr)
+            flat[i] = t
+            g[i] = (lp - lm) / (2 * hs)
+        out.append(g.reshape(arr.shape))
+    return out
+
+
+def test_train_step_is_theta_minus_lr_fd_gradient():
+    # One pgo_train_step must equal theta - lr * g for C, W1, b1, w2 with g the
+    # central finite-difference gradient of the loss (SPEC.md:229, :234): a
+    # sign, scale or index error in the update of any tensor (the embedding
+    # update included) fails here independently of pgo_backward.
+    good, seed = 0, 700
+    while good < 5:
+        seed += 1
+        p, idx, corr = _saturating_fixture(seed)
+        f = oracle.forward(p, idx, corr)
+        m = 1 - f["s"] + f["s_corr"]
+        if min(np.abs(m).min(), np.abs(np.abs(f["a"]) - 1).min(), np.abs(np.abs(f["a_corr"]) - 1).min()) < 1e-4:
+            continue
+        if not (m > 0).any():
+            continue
+        gfd = _fd_grad(p, idx, corr)
+        lr = 0.375
+        q = p.copy()
+        oracle.train_step(q, idx, corr, lr)
+        for name, g, before, after in zip(("C", "W1", "b1", "w2"), gfd, (p.C, p.W1, p.b1, p.w2),
+                                          (q.C, q.W1, q.b1, q.w2)):
+            assert np.abs(g).max() > 0, name
+            step = after - before
+            tol = 1e-5 * lr * np.maximum(np.abs(g), np.abs(g).max() * 1e-3) + 1e-9
+            err = np.abs(step + lr * g)
+            assert (err <= tol).all(), f"{name}: max err {err.max():.3g} (seed {seed})"
+        assert q.b2[0] == p.b2[0]
+        good += 1
