@@ -88,12 +88,34 @@ enum {
   PG_OPT_ACTIVATION = 6, /* value: PG_ACT_HARDTANH (default) or PG_ACT_TANH; applies
                             to pg_train_step* and pg_score from the next call on.
                             PG_EINVAL for any other value. */
-  PG_OPT_REDUCTION = 7   /* value: PG_REDUCE_MEAN (default: L = (1/B) sum_k l_k and
+  PG_OPT_REDUCTION = 7,  /* value: PG_REDUCE_MEAN (default: L = (1/B) sum_k l_k and
                             its gradient, B the global batch; reading G4) or
                             PG_REDUCE_SUM (L = sum_k l_k: the same step as MEAN at
                             lr * B; the reading PAPER.md:197-198 hints at).
                             PG_EINVAL for any other value. */
+  PG_OPT_EXCHANGE = 8    /* value: PG_EXCHANGE_* -- how data-parallel ranks exchange
+                            gradients (after pg_attach_nccl, and in
+                            pg_train_step_group).  Takes effect at the next step. */
 };
+
+/* Data-parallel gradient exchange.  Every
+ * rank first merges its own embedding-gradient rows per row (one entry per
+ * distinct row); then:
+ *   PEER      one kernel per step: each rank's owner CTAs read the other
+ *             ranks' merged rows and dense-gradient sums directly from their
+ *             NCCL symmetric-memory windows over NVLink (load/store
+ *             accessible peers), ready flags pushed by the writers; bytes on
+ *             the wire = the merged rows;
+ *   ALLGATHER ncclAllReduce of the dense gradient + ncclAllGather of the
+ *             merged (row, gradient) records, padded to capacity;
+ *   TABLE     ncclAllReduce of the dense gradient and of a full vocab x dim
+ *             embedding-gradient table;
+ *   AUTO      (default) PEER when every rank is load/store accessible, else
+ *             the cheaper of ALLGATHER and TABLE by bytes received per rank.
+ * PEER and ALLGATHER sum each row's and each dense element's per-rank parts in
+ * rank order on every rank (bit-identical replicas, and bit-identical to each
+ * other); TABLE's sums are NCCL's (identical on all ranks). */
+enum { PG_EXCHANGE_AUTO = 0, PG_EXCHANGE_PEER = 1, PG_EXCHANGE_ALLGATHER = 2, PG_EXCHANGE_TABLE = 3 };
 
 enum { PG_REDUCE_MEAN = 0, PG_REDUCE_SUM = 1 };
 
@@ -183,21 +205,36 @@ pg_status pg_scatter_add_async(float* W, int64_t rows, int32_t cols,
 
 /* Data parallelism over NCCL (one process per GPU).  rank 0 calls
  * pg_nccl_unique_id, the caller broadcasts the 128 bytes (torch.distributed),
- * then every rank calls pg_attach_nccl.  Afterwards pg_train_step exchanges
- * the per-rank dense gradients and the (row, gradient) pairs with
- * ncclAllGather and every rank applies the same update in the same order, so
- * replicas stay bit-identical in PG_SCATTER_DET mode. */
+ * then every rank calls pg_attach_nccl (world == 1 is allowed: a one-rank
+ * communicator, the same code path).  Afterwards pg_train_step is collective:
+ * every rank passes its own shard with the same batch, the gradient is that of
+ * the global mean loss, and the update is exchanged as PG_OPT_EXCHANGE says.
+ * The embedding update is always deterministic in data-parallel steps
+ * (PG_OPT_SCATTER is ignored), so replicas stay bit-identical.  The first step
+ * at a new batch size allocates (collectively) the exchange buffers.
+ * Re-attaching replaces the communicator and frees the exchange buffers. */
 pg_status pg_nccl_unique_id(void* out_128_bytes);
 pg_status pg_attach_nccl(pg_model* m, int rank, int world,
                          const void* nccl_unique_id_128_bytes);
 
+/* The exchange in use (PG_EXCHANGE_*, -1 before the first data-parallel step)
+ * and statistics since the last call with reset != 0: stats[0] = bytes this
+ * rank read from other ranks' records (PEER / group emulation; the NCCL
+ * exchanges report their per-step receive volume times the steps), stats[1]
+ * = the most (row, gradient) entries one owner CTA merged in one step.  Any
+ * pointer may be NULL. */
+pg_status pg_exchange_info(pg_model* m, int* mode, uint64_t* stats2, int reset);
+
 /* pg_train_step_group -- `world` replicas of one model on ONE device take one
  * data-parallel step together: replica r trains on windows
- * idx_all[r*batch_local .. (r+1)*batch_local) (contiguous shards), the per-
- * replica records are exchanged by device copies instead of NCCL, and every
- * replica applies the same update (the arithmetic of the NCCL path, for tests
- * and single-GPU emulation of G ranks).  loss_out (host, may be NULL) gets the
- * global mean loss.  Models used here must not also be attached to NCCL. */
+ * idx_all[r*batch_local .. (r+1)*batch_local) (contiguous shards).  The same
+ * kernels as the NCCL path run; the replicas' exchange windows are one device
+ * buffer (PEER: read in place; ALLGATHER / TABLE: the collectives are
+ * emulated by device copies and rank-order sums), so every replica applies
+ * the same update (tests and single-GPU emulation of G ranks; the exchange
+ * mode is replica 0's PG_OPT_EXCHANGE).  loss_out (host, may be NULL) gets
+ * the global mean loss.  The replicas' own settings (stream, world) are left
+ * as they were; models attached to NCCL are rejected. */
 pg_status pg_train_step_group(pg_model** models, int world, const int32_t* idx_all,
                               const int32_t* corr_all, int32_t batch_local, float lr,
                               float* loss_out);

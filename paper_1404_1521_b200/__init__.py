@@ -27,6 +27,9 @@ PG_OK, PG_EINVAL, PG_ERANGE, PG_ENOMEM, PG_ECUDA, PG_ENCCL, PG_EDIVERGED = range
 PG_SCATTER_DET, PG_SCATTER_ATOMIC = 0, 1
 PG_OPT_SCATTER, PG_OPT_STREAM, PG_OPT_FUSED, PG_OPT_RESERVE, PG_OPT_TRACE, PG_OPT_ACTIVATION = 1, 2, 3, 4, 5, 6
 PG_OPT_REDUCTION = 7
+PG_OPT_EXCHANGE = 8
+PG_EXCHANGE_AUTO, PG_EXCHANGE_PEER, PG_EXCHANGE_ALLGATHER, PG_EXCHANGE_TABLE = 0, 1, 2, 3
+EXCHANGE_NAMES = {-1: "none", 0: "auto", 1: "peer", 2: "allgather", 3: "table"}
 PG_ACT_HARDTANH, PG_ACT_TANH = 0, 1
 PG_REDUCE_MEAN, PG_REDUCE_SUM = 0, 1
 
@@ -34,7 +37,7 @@ EXPORTED = [
     "pg_init", "pg_train_step", "pg_train_step_loss", "pg_score", "pg_free", "pg_last_error",
     "pg_get_params", "pg_set_params", "pg_get_shape", "pg_set_option", "pg_sync",
     "pg_scatter_add", "pg_scatter_add_async", "pg_nccl_unique_id", "pg_attach_nccl",
-    "pg_kernel_launches", "pg_abi_version", "pg_train_step_group",
+    "pg_kernel_launches", "pg_abi_version", "pg_train_step_group", "pg_exchange_info",
 ]
 
 _lib = None
@@ -73,6 +76,7 @@ def lib():
             "pg_kernel_launches": ([P], i64),
             "pg_abi_version": ([], ctypes.c_int),
             "pg_train_step_group": ([P, ctypes.c_int, P, P, i32, f32, P], ctypes.c_int),
+            "pg_exchange_info": ([P, P, P, ctypes.c_int], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -139,10 +143,12 @@ def pg_init(vocab, dim, window, hidden, seed=42):
     h = ctypes.c_void_p()
     _check(lib().pg_init(ctypes.byref(h), int(vocab), int(dim), int(window), int(hidden),
                          int(seed) & 0xFFFFFFFFFFFFFFFF), "pg_init")
+    _SHAPES[_hkey(h)] = int(window)
     return h
 
 
 def pg_free(handle):
+    _SHAPES.pop(_hkey(handle), None)
     lib().pg_free(handle)
 
 
@@ -153,10 +159,44 @@ def pg_set_option(handle, key, value):
 _HOST = "host"
 
 
+def _window_of(handle):
+    n = _SHAPES.get(_hkey(handle))
+    if n is None:
+        n = pg_get_shape(handle)[2]
+    return n
+
+
+def _hkey(handle):
+    return handle.value if hasattr(handle, "value") else int(handle)
+
+
+_SHAPES = {}   # handle -> window (cached by pg_init; pg_get_shape otherwise)
+
+
+def _check_batch(handle, idx_batch, corrupt_idx=None):
+    """The C side reads batch*window ints of idx and batch of corr: mismatched
+    arrays would be out-of-bounds reads, so reject them here (ValueError)."""
+    n = _window_of(handle)
+    if len(idx_batch.shape) == 2:
+        if int(idx_batch.shape[1]) != n:
+            raise ValueError(f"idx_batch has {idx_batch.shape[1]} columns, the model window is {n}")
+        batch = int(idx_batch.shape[0])
+    elif len(idx_batch.shape) == 1:
+        if int(idx_batch.shape[0]) % n:
+            raise ValueError(f"flat idx_batch of {idx_batch.shape[0]} ints is not a multiple of window {n}")
+        batch = int(idx_batch.shape[0]) // n
+    else:
+        raise ValueError("idx_batch must be [batch][window] (or flat batch*window)")
+    if corrupt_idx is not None:
+        if len(corrupt_idx.shape) != 1 or int(corrupt_idx.shape[0]) != batch:
+            raise ValueError(f"corrupt_idx must have shape ({batch},), got {tuple(corrupt_idx.shape)}")
+    return batch
+
+
 def pg_train_step(handle, idx_batch, corrupt_idx, lr, loss_out=_HOST):
     """One SGD step.  loss_out="host" -> blocking, returns the float loss;
     a device float32 tensor -> asynchronous, loss written there; None -> async."""
-    batch = int(corrupt_idx.shape[0])
+    batch = _check_batch(handle, idx_batch, corrupt_idx)
     # `is`, not `==`: comparing a torch tensor with a str costs ~13 us per call
     if loss_out is _HOST or (isinstance(loss_out, str) and loss_out == "host"):
         out = ctypes.c_float()
@@ -170,14 +210,17 @@ def pg_train_step(handle, idx_batch, corrupt_idx, lr, loss_out=_HOST):
 
 
 def pg_train_step_loss(handle, idx_batch, corrupt_idx, lr):
+    batch = _check_batch(handle, idx_batch, corrupt_idx)
     return lib().pg_train_step_loss(handle, _ptr(idx_batch, np.int32), _ptr(corrupt_idx, np.int32),
-                                    int(corrupt_idx.shape[0]), float(lr))
+                                    batch, float(lr))
 
 
 def pg_score(handle, idx_batch, scores_out=None):
-    batch = int(idx_batch.shape[0])
+    batch = _check_batch(handle, idx_batch)
     if scores_out is None:
         scores_out = np.zeros(batch, np.float32)
+    if len(scores_out.shape) != 1 or int(scores_out.shape[0]) < batch:
+        raise ValueError(f"scores_out must hold {batch} floats")
     _check(lib().pg_score(handle, _ptr(idx_batch, np.int32), batch, _ptr(scores_out, np.float32)),
            "pg_score")
     return scores_out
@@ -216,8 +259,14 @@ def pg_sync(handle):
 
 def pg_scatter_add(W, Y, I, mode=PG_SCATTER_DET, stream=None, blocking=True, err_flag=None):
     """W[I[k], :] += Y[k, :] on device tensors."""
+    if len(W.shape) != 2:
+        raise ValueError("W must be 2-D [rows][cols]")
+    if len(I.shape) != 1:
+        raise ValueError("I must be 1-D")
     n = int(I.shape[0])
     rows, cols = int(W.shape[0]), int(W.shape[1])
+    if tuple(Y.shape) != (n, cols) and not (n == 0 and int(np.prod(Y.shape)) == 0):
+        raise ValueError(f"Y must have shape ({n}, {cols}), got {tuple(Y.shape)}")
     s = ctypes.c_void_p(_stream_handle(stream))
     if blocking:
         _check(lib().pg_scatter_add(_ptr(W, np.float32), rows, cols, _ptr(Y, np.float32),
@@ -241,6 +290,16 @@ def pg_attach_nccl(handle, rank, world, unique_id: bytes):
            "pg_attach_nccl")
 
 
+def pg_exchange_info(handle, reset=False):
+    """(exchange in use as a name, bytes read from other ranks, max entries one
+    owner merged) since the last reset."""
+    mode = ctypes.c_int()
+    st = (ctypes.c_uint64 * 2)()
+    _check(lib().pg_exchange_info(handle, ctypes.byref(mode), ctypes.cast(st, ctypes.c_void_p), int(bool(reset))),
+           "pg_exchange_info")
+    return EXCHANGE_NAMES.get(mode.value, str(mode.value)), int(st[0]), int(st[1])
+
+
 def pg_kernel_launches(handle) -> int:
     return int(lib().pg_kernel_launches(handle))
 
@@ -250,7 +309,7 @@ class PolyglotModel:
     """Owns a pg_model handle; methods forward to the C ABI with the torch stream."""
 
     def __init__(self, vocab, dim, window, hidden, seed=42, scatter=PG_SCATTER_DET, stream=None,
-                 fused=True, activation=PG_ACT_HARDTANH, reduction=PG_REDUCE_MEAN):
+                 fused=True, activation=PG_ACT_HARDTANH, reduction=PG_REDUCE_MEAN, exchange=PG_EXCHANGE_AUTO):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("PolyglotModel needs a CUDA device (no CPU fallback)")
@@ -261,6 +320,7 @@ class PolyglotModel:
         pg_set_option(self.handle, PG_OPT_FUSED, 1 if fused else 0)
         pg_set_option(self.handle, PG_OPT_ACTIVATION, activation)
         pg_set_option(self.handle, PG_OPT_REDUCTION, reduction)
+        pg_set_option(self.handle, PG_OPT_EXCHANGE, exchange)
 
     def set_stream(self, stream):
         pg_set_option(self.handle, PG_OPT_STREAM, _stream_handle(stream))
@@ -285,6 +345,9 @@ class PolyglotModel:
 
     def attach_nccl(self, rank, world, uid):
         pg_attach_nccl(self.handle, rank, world, uid)
+
+    def exchange_info(self, reset=False):
+        return pg_exchange_info(self.handle, reset)
 
     def kernel_launches(self):
         return pg_kernel_launches(self.handle)
@@ -314,6 +377,9 @@ def pg_train_step_group(handles, idx_all, corr_all, lr):
     shards of idx_all / corr_all); returns the global mean loss."""
     world = len(handles)
     arr = (ctypes.c_void_p * world)(*[h.value if hasattr(h, "value") else h for h in handles])
+    if int(corr_all.shape[0]) % world:
+        raise ValueError(f"global batch {corr_all.shape[0]} is not divisible by {world} replicas")
+    _check_batch(handles[0], idx_all, corr_all)
     batch_local = int(corr_all.shape[0]) // world
     out = ctypes.c_float()
     _check(lib().pg_train_step_group(ctypes.cast(arr, ctypes.c_void_p), world, _ptr(idx_all, np.int32),

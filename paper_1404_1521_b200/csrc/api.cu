@@ -77,20 +77,26 @@ struct pg_model {
   int in_slot = 0, pending_slot = -1;
   float* d_scores = nullptr;
   int64_t launches = 0;
-  // data parallel
+  // data parallel (pg_attach_nccl): exchange window and NCCL buffers, sized
+  // for batch x_B
   int rank = 0, world = 1;
   void* comm = nullptr;
-  // data-parallel records: send = this rank's, recv = [world][...] gathered
-  float* send_dense = nullptr;
-  int32_t* send_off = nullptr;
-  int32_t* send_rows = nullptr;
-  float* send_vals = nullptr;
-  float* recv_dense = nullptr;
-  int32_t* recv_off = nullptr;
-  int32_t* recv_rows = nullptr;
-  float* recv_vals = nullptr;
-  int64_t dp_cap_B = 0;
-  bool emulated = false;   // group of replicas on one device (pg_train_step_group)
+  int xmode = PG_EXCHANGE_AUTO;   // requested (PG_OPT_EXCHANGE)
+  int xchosen = -1;               // in use for x_B
+  int x_B = 0;
+  XLayout xl{};
+  unsigned char* xwin = nullptr;  // this rank's window (ncclMemAlloc'd + registered for PEER)
+  void* xwin_handle = nullptr;    // ncclWindow_t of the registration (PEER), else null
+  bool xwin_nccl = false;         // xwin came from ncclMemAlloc
+  unsigned char* xbase = nullptr; // rank 0's window in this rank's address space (PEER)
+  size_t xstride = 0;
+  unsigned char* xrecv = nullptr; // ALLGATHER: [world][blk_bytes]
+  float* xdense = nullptr;        // ALLGATHER / TABLE: all-reduced [dense_stride]
+  float* xtable = nullptr;        // TABLE: [V][d] gradient table (kept zero between steps)
+  unsigned* xepoch = nullptr;     // [kMaxSMs] per-CTA step counters
+  unsigned long long* xstats = nullptr;   // [2] exchange statistics (pg_exchange_info)
+  int64_t x_launch_bytes = 0;     // NCCL exchanges: bytes received per step (host-computed)
+  int64_t x_steps = 0;            // NCCL-exchange steps since the last pg_exchange_info reset
 };
 
 // ------------------------------------------------------------------ init kernel
@@ -169,12 +175,37 @@ static PtrKind ptr_kind(const void* p) {
   return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? PTR_DEVICE : PTR_HOST;
 }
 
+// Exchange buffers (data parallel); the window is collective for PEER.
 static void free_dp(pg_model* m) {
-  cudaFree(m->send_dense); cudaFree(m->send_off); cudaFree(m->send_rows); cudaFree(m->send_vals);
-  cudaFree(m->recv_dense); cudaFree(m->recv_off); cudaFree(m->recv_rows); cudaFree(m->recv_vals);
-  m->send_dense = m->recv_dense = m->send_vals = m->recv_vals = nullptr;
-  m->send_off = m->send_rows = m->recv_off = m->recv_rows = nullptr;
-  m->dp_cap_B = 0;
+  if (m->xwin_handle && m->comm) nccl_shim_window_deregister(m->comm, m->xwin_handle);
+  if (m->xwin_nccl) nccl_shim_mem_free(m->xwin);
+  else cudaFree(m->xwin);
+  cudaFree(m->xrecv); cudaFree(m->xdense); cudaFree(m->xtable);
+  m->xwin = m->xrecv = nullptr;
+  m->xdense = m->xtable = nullptr;
+  m->xwin_handle = nullptr;
+  m->xwin_nccl = false;
+  m->xbase = nullptr;
+  m->xstride = 0;
+  m->x_B = 0;
+  m->xchosen = -1;
+}
+
+// Group emulation buffers, owned by replica 0 of a group (keyed by world, B).
+struct GroupX {
+  int world = 0, B = 0, mode = -1;
+  unsigned char* win = nullptr;    // [world][xl.total]
+  unsigned char* recv = nullptr;   // ALLGATHER: [world][blk_bytes]
+  float* dense = nullptr;          // ALLGATHER / TABLE: reduced dense
+  float* table = nullptr;          // TABLE
+  std::vector<unsigned*> epochs;   // per replica
+};
+static std::mutex g_group_mu;
+static std::vector<std::pair<pg_model*, GroupX>> g_groups;
+
+static void free_group(GroupX& gx) {
+  cudaFree(gx.win); cudaFree(gx.recv); cudaFree(gx.dense); cudaFree(gx.table);
+  gx = GroupX{};
 }
 
 static void free_ws(pg_model* m) {
@@ -189,7 +220,7 @@ struct Geometry {
   Layout lay;
 };
 
-static Geometry geometry(const pg_model* m, int B) {
+static Geometry geometry(const pg_model* m, int B, int world = 1) {
   Geometry g{};
   g.P = B < m->num_sms ? B : m->num_sms;
   const int per = (B + g.P - 1) / g.P;
@@ -199,14 +230,14 @@ static Geometry geometry(const pg_model* m, int B) {
   g.NL = g.P * g.R;
   g.dense_len = m->n * m->d * m->h + 2 * m->h;
   g.dense_stride = ((g.dense_len + 2) + 3) & ~3;   // dense | hinge | flags
-  g.lay = make_layout(m->d, m->n, m->h, g.T, step_block_threads(m->d, m->n, m->h, m->fast), g.NL * m->world,
-                      m->fast);
+  g.lay = make_layout(m->d, m->n, m->h, g.T, step_block_threads(m->d, m->n, m->h, m->fast),
+                      g.NL > world ? g.NL : world, m->fast);
   g.smem = (size_t)(g.lay.total1 > g.lay.total2 ? g.lay.total1 : g.lay.total2);
   return g;
 }
 
-static pg_status ensure_ws(pg_model* m, int B) {
-  Geometry g = geometry(m, B);
+static pg_status ensure_ws(pg_model* m, int B, int world = 1) {
+  Geometry g = geometry(m, B, world);
   if (g.smem > m->smem_max)
     return fail(PG_EINVAL, "batch %d needs %zu B of shared memory per CTA (max %zu)", B, g.smem, m->smem_max);
   const int64_t lists = (int64_t)g.NL;
@@ -221,20 +252,6 @@ static pg_status ensure_ws(pg_model* m, int B) {
     CU(cudaMalloc(&m->list_vals, sizeof(float) * L * m->d));
     CU(cudaMalloc(&m->list_off, sizeof(int32_t) * off));
     m->cap_lists = L; m->cap_dense = dense; m->cap_off = off;
-  }
-  if (m->world > 1 && B != m->dp_cap_B) {   // record sizes depend on the exact local batch
-    CU(cudaStreamSynchronize(m->stream));
-    free_dp(m);
-    const int64_t W = m->world, cap = (int64_t)(m->n + 1) * B, offn = (int64_t)g.NL * (g.P + 1);
-    CU(cudaMalloc(&m->send_dense, sizeof(float) * g.dense_stride));
-    CU(cudaMalloc(&m->send_off, sizeof(int32_t) * offn));
-    CU(cudaMalloc(&m->send_rows, sizeof(int32_t) * cap));
-    CU(cudaMalloc(&m->send_vals, sizeof(float) * cap * m->d));
-    CU(cudaMalloc(&m->recv_dense, sizeof(float) * g.dense_stride * W));
-    CU(cudaMalloc(&m->recv_off, sizeof(int32_t) * offn * W));
-    CU(cudaMalloc(&m->recv_rows, sizeof(int32_t) * cap * W));
-    CU(cudaMalloc(&m->recv_vals, sizeof(float) * cap * m->d * W));
-    m->dp_cap_B = B;
   }
   if (B > m->cap_in) {
     CU(cudaStreamSynchronize(m->stream));
@@ -270,6 +287,7 @@ static pg_status status_from_flags(int flags, unsigned long long bad, const char
     return fail(PG_ERANGE, "%s: index out of range at flat position %lld (value %d); no parameter was modified",
                 what, pos, val);
   }
+  if (flags & 4) return fail(PG_ENCCL, "%s: a data-parallel rank did not publish its gradients in time; no parameter was modified", what);
   if (flags & 2) return fail(PG_EDIVERGED, "%s: non-finite loss; no parameter was modified", what);
   return PG_OK;
 }
@@ -343,8 +361,16 @@ extern "C" void pg_free(pg_model* m) {
   cudaSetDevice(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
   else cudaDeviceSynchronize();
+  free_dp(m);
   if (m->comm) nccl_shim_destroy(m->comm);
+  m->comm = nullptr;
   free_ws(m);
+  cudaFree(m->xepoch); cudaFree(m->xstats);
+  {
+    std::lock_guard<std::mutex> lk(g_group_mu);
+    for (size_t i = 0; i < g_groups.size(); ++i)
+      if (g_groups[i].first == m) { free_group(g_groups[i].second); g_groups.erase(g_groups.begin() + i); break; }
+  }
   cudaFree(m->C); cudaFree(m->W1); cudaFree(m->W1T); cudaFree(m->b1); cudaFree(m->w2); cudaFree(m->b2);
   cudaFree(m->st); cudaFreeHost(m->st_host);
   if (m->copy_stream) cudaStreamSynchronize(m->copy_stream);
@@ -355,7 +381,6 @@ extern "C" void pg_free(pg_model* m) {
   }
   if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
   cudaFree(m->d_scores);
-  free_dp(m);
   delete m;
 }
 
@@ -392,6 +417,18 @@ extern "C" pg_status pg_set_option(pg_model* m, int key, int64_t value) {
       if (value != PG_REDUCE_MEAN && value != PG_REDUCE_SUM)
         return fail(PG_EINVAL, "PG_OPT_REDUCTION: unknown reduction %lld", (long long)value);
       m->reduce_sum = value == PG_REDUCE_SUM;
+      return PG_OK;
+    case PG_OPT_EXCHANGE:
+      if (value < PG_EXCHANGE_AUTO || value > PG_EXCHANGE_TABLE)
+        return fail(PG_EINVAL, "PG_OPT_EXCHANGE: unknown exchange %lld", (long long)value);
+      if (m->xmode != (int)value) {
+        m->xmode = (int)value;
+        if (m->x_B) {   // re-chosen (collectively) at the next step
+          if (pg_status s = set_device(m)) return s;
+          CU(cudaStreamSynchronize(m->stream));
+          free_dp(m);
+        }
+      }
       return PG_OK;
     case PG_OPT_TRACE:   // device buffer of [P][32] u64 stage stamps (libpg_trace.so), 0 = off
       m->trace = reinterpret_cast<unsigned long long*>(value);
@@ -518,8 +555,7 @@ extern "C" pg_status pg_train_step(pg_model* m, const int32_t* idx_batch, const 
   CU(cudaMemcpyAsync(m->st_host, m->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
   *loss_out = m->st_host->last_loss;
-  const int flags = m->world > 1 ? m->st_host->rank_flags : m->st_host->last_flags;
-  return status_from_flags(flags, m->st_host->last_bad, "pg_train_step");
+  return status_from_flags(m->st_host->last_flags, m->st_host->last_bad, "pg_train_step");
 }
 
 extern "C" float pg_train_step_loss(pg_model* m, const int32_t* idx_batch, const int32_t* corrupt_idx,
@@ -575,43 +611,203 @@ extern "C" pg_status pg_sync(pg_model* m) {
 
 // ------------------------------------------------------------------ step launch
 static StepParams make_params(pg_model* m, const Geometry& g, const int32_t* idx, const int32_t* corr, int B,
-                              float lr, float* loss_dev) {
+                              float lr, float* loss_dev, int world = 1) {
   StepParams p{};
   p.C = m->C; p.W1 = m->W1; p.W1T = m->W1T; p.b1 = m->b1; p.w2 = m->w2; p.b2 = m->b2;
   p.V = m->V; p.d = m->d; p.n = m->n; p.h = m->h;
   p.idx = idx; p.corr = corr; p.B = B;
-  p.inv_B = m->reduce_sum ? 1.0f : 1.0f / (float)((int64_t)B * m->world);
+  p.inv_B = m->reduce_sum ? 1.0f : 1.0f / (float)((int64_t)B * world);
   p.act = m->act;
   p.lr = lr;
   p.P = g.P; p.R = g.R; p.T = g.T; p.cap = g.cap;
   p.dense_part = m->dense_part;
   p.dense_len = g.dense_len; p.dense_stride = g.dense_stride;
   p.list_rows = m->list_rows; p.list_vals = m->list_vals; p.list_off = m->list_off;
-  p.Ptot = g.P; p.NLtot = g.NL;
+  p.NL = g.NL;
   p.st = m->st;
   p.loss_out = loss_dev;
   p.mode = m->mode;
   p.smem_bytes = (int)g.smem;
-  p.LPR = g.NL;
-  p.list_stride = g.cap;
-  p.rank_stride = 0;
-  p.flags_from_records = 0;
-  p.send_dense = m->send_dense;
-  p.send_off = m->send_off;
-  p.send_rows = m->send_rows;
-  p.send_vals = m->send_vals;
   p.lay = g.lay;
   p.trace = m->trace;
+  p.world = world;
+  p.rank = 0;
   return p;
 }
 
-pg_status dp_step(pg_model* m, const Geometry& g, StepParams& p);
+static pg_status run_step(pg_model* m, const int32_t* idx, const int32_t* corr, int B, float lr,
+                          float* loss_dev);
+
+// ------------------------------------------------------------------ data parallel
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Window of one rank for batch B: ready flags, two parity
+// blocks [headers | rows | values], two dense sums.
+static XLayout x_layout(const pg_model* m, const Geometry& g, int B) {
+  XLayout xl{};
+  const size_t cap = (size_t)(m->n + 1) * B;
+  size_t o = 0;
+  xl.flags = o;  o = align_up(o + sizeof(unsigned) * kMaxRanks * kMaxSMs, 4096);
+  xl.rows = align_up(sizeof(XHdr) * kMaxSMs, 256);
+  xl.vals = align_up(xl.rows + sizeof(int32_t) * cap, 256);
+  xl.blk_bytes = align_up(xl.vals + sizeof(float) * cap * m->d, 256);
+  for (int k = 0; k < 2; ++k) { xl.blk[k] = o; o = align_up(o + xl.blk_bytes, 4096); }
+  for (int k = 0; k < 2; ++k) { xl.dense[k] = o; o = align_up(o + sizeof(float) * g.dense_stride, 4096); }
+  xl.total = align_up(o, 1 << 21);
+  return xl;
+}
+
+static size_t allgather_bytes(const pg_model* m, const XLayout& xl, int world) {
+  return (size_t)(world - 1) * xl.blk_bytes;
+}
+static size_t table_bytes(const pg_model* m, int world) {   // ring all-reduce: 2 (G-1)/G of the table
+  return (size_t)(2.0 * (world - 1) / world * (double)m->V * m->d * sizeof(float));
+}
+
+// Cost model (SURVEY.md §8(e) "chosen by measured cost"): the peer window
+// moves only the merged rows and needs no collective launch, so it wins when
+// available; otherwise the fewer bytes received per rank.
+static int choose_exchange(const pg_model* m, const XLayout& xl, int world, bool peer_ok) {
+  if (m->xmode != PG_EXCHANGE_AUTO) return m->xmode;
+  if (peer_ok) return PG_EXCHANGE_PEER;
+  return allgather_bytes(m, xl, world) <= table_bytes(m, world) ? PG_EXCHANGE_ALLGATHER : PG_EXCHANGE_TABLE;
+}
+
+static pg_status ensure_x_small(pg_model* m) {
+  if (!m->xepoch) {
+    CU(cudaMalloc(&m->xepoch, sizeof(unsigned) * kMaxSMs));
+    CU(cudaMemset(m->xepoch, 0, sizeof(unsigned) * kMaxSMs));
+  }
+  if (!m->xstats) {
+    CU(cudaMalloc(&m->xstats, sizeof(unsigned long long) * 2));
+    CU(cudaMemset(m->xstats, 0, sizeof(unsigned long long) * 2));
+  }
+  return PG_OK;
+}
+
+// Collective on first use of a batch size (every rank calls pg_train_step with
+// the same batch): window, then the mode's buffers.
+static pg_status ensure_dp(pg_model* m, int B) {
+  if (m->x_B == B && m->xwin) return PG_OK;
+  CU(cudaStreamSynchronize(m->stream));
+  free_dp(m);
+  if (pg_status s = ensure_x_small(m)) return s;
+  const Geometry g = geometry(m, B, m->world);
+  m->xl = x_layout(m, g, B);
+  std::string err;
+  bool peer_ok = false;
+  const bool want_peer = m->xmode == PG_EXCHANGE_AUTO || m->xmode == PG_EXCHANGE_PEER;
+  if (want_peer && nccl_shim_lsa_size(m->comm) == m->world) {
+    void* buf = nullptr;
+    void* win = nullptr;
+    if (!nccl_shim_mem_alloc(&buf, m->xl.total, &err)) {
+      m->xwin = static_cast<unsigned char*>(buf);
+      m->xwin_nccl = true;
+      if (cudaMemset(m->xwin, 0, m->xl.total) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess &&
+          !nccl_shim_window_register(m->comm, buf, m->xl.total, &win, &err)) {
+        m->xwin_handle = win;
+        std::vector<unsigned long long> ptrs(m->world);
+        if (!nccl_lsa_pointers(win, m->world, ptrs.data(), &err)) {
+          bool uniform = ptrs[m->rank] == reinterpret_cast<unsigned long long>(m->xwin) || true;
+          const unsigned long long stride = m->world > 1 ? ptrs[1] - ptrs[0] : m->xl.total;
+          for (int r = 1; r < m->world; ++r) uniform &= ptrs[r] - ptrs[r - 1] == stride;
+          if (uniform) {
+            m->xbase = reinterpret_cast<unsigned char*>(ptrs[0]);
+            m->xstride = stride;
+            peer_ok = true;
+          }
+        }
+      }
+    }
+    cudaGetLastError();
+  }
+  if (m->xmode == PG_EXCHANGE_PEER && !peer_ok)
+    return fail(PG_ENCCL, "PG_EXCHANGE_PEER: no load/store-accessible symmetric window (%s)", err.c_str());
+  m->xchosen = choose_exchange(m, m->xl, m->world, peer_ok);
+  if (m->xchosen != PG_EXCHANGE_PEER && !m->xwin) {
+    CU(cudaMalloc(&m->xwin, m->xl.total));
+    CU(cudaMemset(m->xwin, 0, m->xl.total));
+  }
+  if (m->xchosen == PG_EXCHANGE_ALLGATHER) CU(cudaMalloc(&m->xrecv, m->xl.blk_bytes * (size_t)m->world));
+  if (m->xchosen != PG_EXCHANGE_PEER) CU(cudaMalloc(&m->xdense, sizeof(float) * g.dense_stride));
+  if (m->xchosen == PG_EXCHANGE_TABLE) {
+    CU(cudaMalloc(&m->xtable, sizeof(float) * (size_t)m->V * m->d));
+    CU(cudaMemset(m->xtable, 0, sizeof(float) * (size_t)m->V * m->d));
+  }
+  m->x_launch_bytes = m->xchosen == PG_EXCHANGE_ALLGATHER ? (int64_t)allgather_bytes(m, m->xl, m->world)
+                      : m->xchosen == PG_EXCHANGE_TABLE   ? (int64_t)table_bytes(m, m->world)
+                                                          : 0;
+  m->x_B = B;
+  CU(cudaDeviceSynchronize());
+  return PG_OK;
+}
+
+static void set_x(StepParams& p, pg_model* m, int rank, int world) {
+  p.world = world;
+  p.rank = rank;
+  p.xl = m->xl;
+  p.xcap = (m->n + 1) * p.B;
+  p.xepoch = m->xepoch;
+  p.xstats = m->xstats;
+  p.mode = PG_SCATTER_DET;
+}
+
+// Data-parallel step over NCCL (one process per GPU).
+static pg_status dp_step(pg_model* m, const int32_t* idx, const int32_t* corr, int B, float lr, float* loss_dev) {
+  if (!m->comm) return fail(PG_ENCCL, "data-parallel step without a communicator");
+  if (pg_status s = ensure_dp(m, B)) return s;
+  const Geometry g = geometry(m, B, m->world);
+  StepParams p = make_params(m, g, idx, corr, B, lr, loss_dev, m->world);
+  set_x(p, m, m->rank, m->world);
+  p.xwin = m->xwin;
+  int l = 0;
+  std::string err;
+  if (m->xchosen == PG_EXCHANGE_PEER) {   // one kernel: phase 1, publish, wait, merge
+    p.xbase = m->xbase;
+    p.xstride = m->xstride;
+    p.xpeer = 1;
+    launch_step_phases(p, 1 | 8 | 16, m->fast, m->stream, &l);
+    m->launches += l;
+    CU(cudaGetLastError());
+    return PG_OK;
+  }
+  p.xgathered = 1;
+  launch_step_phases(p, 1 | 8, m->fast, m->stream, &l);
+  CU(cudaGetLastError());
+  int rc = nccl_shim_group(true, &err);
+  bool opened = rc == 0;
+  float* dense_w = reinterpret_cast<float*>(m->xwin + m->xl.dense[0]);
+  if (!rc) rc = nccl_shim_allreduce_sum_f32(dense_w, m->xdense, (size_t)g.dense_stride, m->comm, m->stream, &err);
+  if (!rc && m->xchosen == PG_EXCHANGE_ALLGATHER)
+    rc = nccl_shim_allgather_bytes(m->xwin + m->xl.blk[0], m->xrecv, m->xl.blk_bytes, m->comm, m->stream, &err);
+  if (opened) {
+    std::string e2;
+    if (nccl_shim_group(false, &e2) && !rc) { rc = 1; err = e2; }
+  }
+  if (rc) return fail(PG_ENCCL, "%s", err.c_str());
+  p.xdense = m->xdense;
+  m->x_steps += 1;
+  if (m->xchosen == PG_EXCHANGE_ALLGATHER) {
+    p.xbase = m->xrecv;
+    p.xstride = m->xl.blk_bytes;
+    launch_step_phases(p, 16, m->fast, m->stream, &l);
+  } else {   // TABLE
+    launch_dp_table(p, m->xtable, 0, m->num_sms, m->stream, &l);
+    CU(cudaGetLastError());
+    if (nccl_shim_allreduce_sum_f32(m->xtable, m->xtable, (size_t)m->V * m->d, m->comm, m->stream, &err))
+      return fail(PG_ENCCL, "%s", err.c_str());
+    launch_dp_table(p, m->xtable, 2, m->num_sms, m->stream, &l);
+  }
+  m->launches += l;
+  CU(cudaGetLastError());
+  return PG_OK;
+}
 
 static pg_status run_step(pg_model* m, const int32_t* idx, const int32_t* corr, int B, float lr,
                           float* loss_dev) {
+  if (m->comm) return dp_step(m, idx, corr, B, lr, loss_dev);
   const Geometry g = geometry(m, B);
   StepParams p = make_params(m, g, idx, corr, B, lr, loss_dev);
-  if (m->world > 1 && !m->emulated) return dp_step(m, g, p);
   int l = 0;
   launch_step(p, m->fused, m->fast, m->stream, &l);
   m->launches += l;
@@ -619,118 +815,132 @@ static pg_status run_step(pg_model* m, const int32_t* idx, const int32_t* corr, 
   return PG_OK;
 }
 
-// ------------------------------------------------------------------ data parallel (NCCL)
-// Phase 2 parameters over the gathered records of `world` ranks.
-static StepParams record_params(const pg_model* m, const Geometry& g, const StepParams& p) {
-  StepParams q = p;
-  const int W = m->world;
-  q.dense_part = m->recv_dense;
-  q.dense_stride = g.dense_stride;
-  q.Ptot = W;
-  q.list_off = m->recv_off;
-  q.list_rows = m->recv_rows;
-  q.list_vals = m->recv_vals;
-  q.NLtot = g.NL * W;
-  q.LPR = g.NL;
-  q.list_stride = 0;
-  q.rank_stride = (m->n + 1) * p.B;
-  q.flags_from_records = 1;
-  return q;
+// Rank-order sum of `world` float vectors spaced `stride` bytes apart (the
+// all-reduce of the emulated NCCL exchanges).
+__global__ void sum_ranks_kernel(const unsigned char* base, size_t stride, int world, int n, float* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int r = 0; r < world; ++r) acc += reinterpret_cast<const float*>(base + (size_t)r * stride)[i];
+    out[i] = acc;
+  }
 }
 
-// Data-parallel step: phase 1 + this rank's compact record in
-// one cooperative kernel, one grouped NCCL all-gather of the records, then the
-// same phase 2 over all ranks' records on every rank -- identical inputs in an
-// identical order, so replicas stay bit-identical in DET mode.
-pg_status dp_step(pg_model* m, const Geometry& g, StepParams& p) {
-  if (!m->comm) return fail(PG_ENCCL, "data-parallel step without a communicator");
-  int l = 0;
-  launch_step_phases(p, 1 | 4, m->fast, m->stream, &l);
-  CU(cudaGetLastError());
-  const int64_t cap = (int64_t)(m->n + 1) * p.B, offn = (int64_t)g.NL * (g.P + 1);
-  std::string err;
-  if (nccl_shim_group(true, &err) ||
-      nccl_shim_allgather_f32(m->send_dense, m->recv_dense, (size_t)g.dense_stride, m->comm, m->stream, &err) ||
-      nccl_shim_allgather_f32(reinterpret_cast<float*>(m->send_off), reinterpret_cast<float*>(m->recv_off),
-                              (size_t)offn, m->comm, m->stream, &err) ||
-      nccl_shim_allgather_f32(reinterpret_cast<float*>(m->send_rows), reinterpret_cast<float*>(m->recv_rows),
-                              (size_t)cap, m->comm, m->stream, &err) ||
-      nccl_shim_allgather_f32(m->send_vals, m->recv_vals, (size_t)(cap * m->d), m->comm, m->stream, &err) ||
-      nccl_shim_group(false, &err))
-    return fail(PG_ENCCL, "%s", err.c_str());
-  const StepParams q = record_params(m, g, p);
-  launch_step_phases(q, 2, m->fast, m->stream, &l);
-  m->launches += l;
-  CU(cudaGetLastError());
-  return PG_OK;
-}
-
-// Replicas of one model on ONE device exchanging records by device copies: the
-// data-parallel arithmetic of dp_step without NCCL (tests, single-GPU runs).
+// Replicas of one model on ONE device (pg_train_step_group): the kernels of
+// the data-parallel path, the collectives emulated on the device.
 extern "C" pg_status pg_train_step_group(pg_model** ms, int world, const int32_t* idx_all,
                                          const int32_t* corr_all, int32_t batch_local, float lr,
                                          float* loss_out) {
-  if (!ms || world < 1) return fail(PG_EINVAL, "pg_train_step_group: bad arguments");
+  if (!ms || world < 1 || world > kMaxRanks) return fail(PG_EINVAL, "pg_train_step_group: bad arguments");
   if (!idx_all || !corr_all) return fail(PG_EINVAL, "pg_train_step_group: null index pointer");
   if (batch_local < 1) return fail(PG_EINVAL, "pg_train_step_group: empty batch");
   if (!std::isfinite(lr) || !(lr > 0.f)) return fail(PG_EINVAL, "pg_train_step_group: lr must be finite and > 0");
   for (int r = 0; r < world; ++r) {
     if (pg_status s = check_model(ms[r])) return s;
     if (ms[r]->comm) return fail(PG_EINVAL, "pg_train_step_group: model %d has an NCCL communicator", r);
-    if (ms[r]->d != ms[0]->d || ms[r]->n != ms[0]->n || ms[r]->h != ms[0]->h || ms[r]->V != ms[0]->V)
-      return fail(PG_EINVAL, "pg_train_step_group: shape mismatch");
-    if (ms[r]->world != world) { ms[r]->world = world; ms[r]->rank = r; free_ws(ms[r]); free_dp(ms[r]); }
-    ms[r]->emulated = true;
-    if (pg_status s = set_device(ms[r])) return s;
-    if (pg_status s = ensure_ws(ms[r], batch_local)) return s;
+    if (ms[r]->d != ms[0]->d || ms[r]->n != ms[0]->n || ms[r]->h != ms[0]->h || ms[r]->V != ms[0]->V ||
+        ms[r]->device != ms[0]->device)
+      return fail(PG_EINVAL, "pg_train_step_group: shape or device mismatch");
+    for (int k = 0; k < r; ++k)
+      if (ms[k] == ms[r]) return fail(PG_EINVAL, "pg_train_step_group: replica %d repeated", r);
   }
   pg_model* m0 = ms[0];
+  if (pg_status s = set_device(m0)) return s;
+  for (int r = 0; r < world; ++r) {
+    if (pg_status s = ensure_ws(ms[r], batch_local, world)) return s;
+    if (pg_status s = ensure_x_small(ms[r])) return s;
+  }
   const int n = m0->n;
-  const Geometry g = geometry(m0, batch_local);
-  // phase 1 + records, one replica after another on replica 0's stream
+  const Geometry g = geometry(m0, batch_local, world);
+  const XLayout xl = x_layout(m0, g, batch_local);
+  const int mode = m0->xmode == PG_EXCHANGE_AUTO ? PG_EXCHANGE_PEER : m0->xmode;
+  std::lock_guard<std::mutex> lk(g_group_mu);
+  GroupX* gx = nullptr;
+  for (auto& e : g_groups)
+    if (e.first == m0) gx = &e.second;
+  if (!gx) { g_groups.emplace_back(m0, GroupX{}); gx = &g_groups.back().second; }
+  if (gx->world != world || gx->B != batch_local || gx->mode != mode) {
+    CU(cudaDeviceSynchronize());
+    free_group(*gx);
+    CU(cudaMalloc(&gx->win, xl.total * world));
+    CU(cudaMemset(gx->win, 0, xl.total * world));
+    if (mode == PG_EXCHANGE_ALLGATHER) CU(cudaMalloc(&gx->recv, xl.blk_bytes * world));
+    if (mode != PG_EXCHANGE_PEER) CU(cudaMalloc(&gx->dense, sizeof(float) * g.dense_stride));
+    if (mode == PG_EXCHANGE_TABLE) {
+      CU(cudaMalloc(&gx->table, sizeof(float) * (size_t)m0->V * m0->d));
+      CU(cudaMemset(gx->table, 0, sizeof(float) * (size_t)m0->V * m0->d));
+    }
+    gx->world = world; gx->B = batch_local; gx->mode = mode;
+    for (int r = 0; r < world; ++r) CU(cudaMemset(ms[r]->xepoch, 0, sizeof(unsigned) * kMaxSMs));
+  }
+  m0->xchosen = mode;
+  cudaStream_t s0 = m0->stream;
+  // phase 1 + publish, replica after replica on replica 0's stream
   std::vector<StepParams> ps(world);
   for (int r = 0; r < world; ++r) {
     pg_model* m = ms[r];
     const int32_t *di = nullptr, *dc = nullptr;
-    m->stream = m0->stream;
-    if (pg_status s = stage_inputs(m, idx_all + (size_t)r * batch_local * n, corr_all + (size_t)r * batch_local,
-                                   batch_local, &di, &dc))
-      return s;
-    ps[r] = make_params(m, g, di, dc, batch_local, lr, nullptr);
-    int l = 0;
-    launch_step_phases(ps[r], 1 | 4, m->fast, m->stream, &l);
-    m->launches += l;
-    CU(cudaGetLastError());
-    if (pg_status s = consume_inputs(m)) return s;
-  }
-  // "all-gather": every replica receives every replica's record
-  const int64_t cap = (int64_t)(n + 1) * batch_local, offn = (int64_t)g.NL * (g.P + 1);
-  for (int dst = 0; dst < world; ++dst)
-    for (int src = 0; src < world; ++src) {
-      pg_model* a = ms[dst];
-      pg_model* b = ms[src];
-      cudaStream_t s = m0->stream;
-      CU(cudaMemcpyAsync(a->recv_dense + (size_t)src * g.dense_stride, b->send_dense, sizeof(float) * g.dense_stride,
-                         cudaMemcpyDeviceToDevice, s));
-      CU(cudaMemcpyAsync(a->recv_off + (size_t)src * offn, b->send_off, sizeof(int32_t) * offn,
-                         cudaMemcpyDeviceToDevice, s));
-      CU(cudaMemcpyAsync(a->recv_rows + (size_t)src * cap, b->send_rows, sizeof(int32_t) * cap,
-                         cudaMemcpyDeviceToDevice, s));
-      CU(cudaMemcpyAsync(a->recv_vals + (size_t)src * cap * a->d, b->send_vals, sizeof(float) * cap * a->d,
-                         cudaMemcpyDeviceToDevice, s));
+    cudaStream_t own = m->stream;
+    m->stream = s0;   // staging orders the copies before the launch on s0
+    pg_status st = stage_inputs(m, idx_all + (size_t)r * batch_local * n, corr_all + (size_t)r * batch_local,
+                                batch_local, &di, &dc);
+    if (!st) {
+      ps[r] = make_params(m, g, di, dc, batch_local, lr, nullptr, world);
+      set_x(ps[r], m, r, world);
+      ps[r].xl = xl;
+      ps[r].xwin = gx->win + (size_t)r * xl.total;
+      ps[r].xbase = gx->win;
+      ps[r].xstride = xl.total;
+      ps[r].xpeer = mode == PG_EXCHANGE_PEER;
+      ps[r].xgathered = mode != PG_EXCHANGE_PEER;
+      int l = 0;
+      launch_step_phases(ps[r], 1 | 8, m->fast, s0, &l);
+      m->launches += l;
+      if (cudaGetLastError() != cudaSuccess) st = fail(PG_ECUDA, "pg_train_step_group: launch failed");
+      if (!st) st = consume_inputs(m);
     }
+    m->stream = own;
+    if (st) return st;
+  }
+  // the "collectives"
+  int l0 = 0;
+  if (mode != PG_EXCHANGE_PEER) {
+    sum_ranks_kernel<<<m0->num_sms, 256, 0, s0>>>(gx->win + xl.dense[0], xl.total, world, g.dense_stride, gx->dense);
+    ++l0;
+  }
+  if (mode == PG_EXCHANGE_ALLGATHER)
+    for (int r = 0; r < world; ++r)
+      CU(cudaMemcpyAsync(gx->recv + (size_t)r * xl.blk_bytes, gx->win + (size_t)r * xl.total + xl.blk[0], xl.blk_bytes,
+                         cudaMemcpyDeviceToDevice, s0));
   for (int r = 0; r < world; ++r) {
-    const StepParams q = record_params(ms[r], g, ps[r]);
+    StepParams& q = ps[r];
     int l = 0;
-    launch_step_phases(q, 2, ms[r]->fast, m0->stream, &l);
+    if (mode == PG_EXCHANGE_TABLE) {
+      q.xdense = gx->dense;
+      launch_dp_table(q, gx->table, 0, m0->num_sms, s0, &l);   // every replica adds into the shared table
+    } else {
+      if (mode == PG_EXCHANGE_ALLGATHER) {
+        q.xdense = gx->dense;
+        q.xbase = gx->recv;
+        q.xstride = xl.blk_bytes;
+      }
+      launch_step_phases(q, 16, ms[r]->fast, s0, &l);
+    }
     ms[r]->launches += l;
     CU(cudaGetLastError());
   }
+  if (mode == PG_EXCHANGE_TABLE)
+    for (int r = 0; r < world; ++r) {   // apply; the last replica re-zeroes the shared table
+      int l = 0;
+      launch_dp_table(ps[r], gx->table, r + 1 < world ? 1 : 2, m0->num_sms, s0, &l);
+      ms[r]->launches += l;
+      CU(cudaGetLastError());
+    }
+  m0->launches += l0;
   if (!loss_out) return PG_OK;
-  CU(cudaMemcpyAsync(m0->st_host, m0->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, m0->stream));
-  CU(cudaStreamSynchronize(m0->stream));
+  CU(cudaMemcpyAsync(m0->st_host, m0->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s0));
+  CU(cudaStreamSynchronize(s0));
   *loss_out = m0->st_host->last_loss;
-  return status_from_flags(m0->st_host->rank_flags, m0->st_host->last_bad, "pg_train_step_group");
+  return status_from_flags(m0->st_host->last_flags, m0->st_host->last_bad, "pg_train_step_group");
 }
 
 extern "C" pg_status pg_nccl_unique_id(void* out) {
@@ -742,17 +952,36 @@ extern "C" pg_status pg_nccl_unique_id(void* out) {
 
 extern "C" pg_status pg_attach_nccl(pg_model* m, int rank, int world, const void* uid) {
   if (pg_status s = check_model(m)) return s;
-  if (!uid || world < 1 || rank < 0 || rank >= world) return fail(PG_EINVAL, "pg_attach_nccl: bad rank/world");
-  if (world == 1) return PG_OK;
+  if (!uid || world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
+    return fail(PG_EINVAL, "pg_attach_nccl: bad rank/world (world <= %d)", kMaxRanks);
   if (pg_status s = set_device(m)) return s;
+  CU(cudaStreamSynchronize(m->stream));
   std::string err;
   void* comm = nullptr;
   if (nccl_shim_init(&comm, rank, world, uid, &err)) return fail(PG_ENCCL, "%s", err.c_str());
+  free_dp(m);   // window / buffers belong to the old communicator
   if (m->comm) nccl_shim_destroy(m->comm);
   m->comm = comm;
   m->rank = rank;
   m->world = world;
-  free_ws(m);   // record layout depends on world
+  free_ws(m);   // geometry depends on world
+  if (m->xepoch) CU(cudaMemset(m->xepoch, 0, sizeof(unsigned) * kMaxSMs));
+  return PG_OK;
+}
+
+extern "C" pg_status pg_exchange_info(pg_model* m, int* mode, uint64_t* stats2, int reset) {
+  if (pg_status s = check_model(m)) return s;
+  if (mode) *mode = m->xchosen;
+  if (pg_status s = set_device(m)) return s;
+  if (stats2 || reset) {
+    if (pg_status s = ensure_x_small(m)) return s;
+    unsigned long long h[2] = {0, 0};
+    CU(cudaStreamSynchronize(m->stream));
+    CU(cudaMemcpy(h, m->xstats, sizeof h, cudaMemcpyDeviceToHost));
+    h[0] += (unsigned long long)(m->x_launch_bytes * m->x_steps);
+    if (stats2) { stats2[0] = h[0]; stats2[1] = h[1]; }
+    if (reset) { CU(cudaMemset(m->xstats, 0, sizeof h)); m->x_steps = 0; }
+  }
   return PG_OK;
 }
 

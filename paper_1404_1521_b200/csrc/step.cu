@@ -39,10 +39,6 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
-__device__ __forceinline__ size_t list_index(const StepParams& p, int L, int off) {
-  return (size_t)(L / p.LPR) * p.rank_stride + (size_t)(L % p.LPR) * p.list_stride + off;
-}
-
 // Optional phase timestamps for profiling (PG_OPT_TRACE; thread 0 of each CTA).
 // Phase stamps for scripts/trace_step.py: compiled only into the instrumented
 // library variant (PG_TRACE, libpg_trace.so) -- the production kernel carries
@@ -1059,7 +1055,7 @@ __device__ __forceinline__ DenseSlice dense_slice(const StepParams& p) {
   return {(int)((long long)blockIdx.x * NQ / G), (int)((long long)(blockIdx.x + 1) * NQ / G)};
 }
 
-// Fixed-order reduction of quads [qb, qb+nq) over the Ptot records: thread
+// Fixed-order reduction of quads [qb, qb+nq) over the P records: thread
 // (quad qi, group g) sums records g, g+G, ... (4 loads in flight).
 __device__ __forceinline__ float4 dense_partial(const StepParams& p, int qb, int nq, int groups) {
   const int qi = threadIdx.x % nq, g = threadIdx.x / nq;
@@ -1067,12 +1063,12 @@ __device__ __forceinline__ float4 dense_partial(const StepParams& p, int qb, int
   if (g >= groups) return acc;
   const float* base = p.dense_part + 4 * (qb + qi);
   #pragma unroll 1
-  for (int r0 = g; r0 < p.Ptot; r0 += 8 * groups) {   // 8 loads in flight, summed in record order
+  for (int r0 = g; r0 < p.P; r0 += 8 * groups) {   // 8 loads in flight, summed in record order
     float4 v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int r = r0 + k * groups;
-      v[k] = r < p.Ptot ? ldcg4(base + (size_t)r * p.dense_stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[k] = r < p.P ? ldcg4(base + (size_t)r * p.dense_stride) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) { acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w; }
@@ -1196,12 +1192,18 @@ __device__ __forceinline__ void fb_segsum(float* stage, float* carry, int d, int
 // Sorted fallback for owners with more than MCAP entries (pathological index
 // patterns): windows of whole lists, bitonic sort by (row, list), segment sums
 // in list order with a carry across staged sub-batches.
-__device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
+// emit_rows == nullptr: C[row] += -lr * total; else the (row, total) pairs are
+// written to emit_rows / emit_vals from index 0 on (a row whose entries
+// straddle two key windows is emitted twice, its partials in order) and the
+// number written is returned.
+__device__ int scatter_det_sorted(const StepParams& p, unsigned char* sm, const Lists& ls,
+                                  int32_t* emit_rows = nullptr, float* emit_vals = nullptr) {
   const Layout& lay = p.lay;
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
-  const int d = p.d, NL = p.NLtot;
+  const int d = p.d, NL = ls.xstride ? p.world : p.NL;
   const int* lbase = reinterpret_cast<const int*>(sm + lay.lbase);
   const int* loff = reinterpret_cast<const int*>(sm + lay.loff);
+  int emitted = 0;
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(sm + lay.keys);
   int* seg = reinterpret_cast<int*>(sm + lay.seg);
   float* stage = reinterpret_cast<float*>(sm + lay.stagefb);
@@ -1227,13 +1229,12 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
           }
           const int L = lo;
           const int rel = base + e - lbase[L];   // offset inside the owner bucket (< 256)
-          // low word: the entry's position in the list storage, which grows
-          // with (list, offset) in both layouts (per-CTA lists; DP records,
-          // rank-major with compacted owner buckets), so sorting by the key
-          // orders each row's entries by (list, offset) as before
-          const size_t li = list_index(p, L, loff[L] + rel);
-          const unsigned row = (unsigned)__ldcg(p.list_rows + li);
-          keys[e] = ((unsigned long long)row << 32) | (unsigned long long)(unsigned)li;
+          // low word: the entry code, which grows with (list, offset) in both
+          // layouts (per-CTA lists; ranked records), so sorting by the key
+          // orders each row's entries by (list, offset)
+          const unsigned li = ls.code(L, loff[L] + rel);
+          const unsigned row = (unsigned)__ldcg(ls.row(li));
+          keys[e] = ((unsigned long long)row << 32) | (unsigned long long)li;
         } else {
           keys[e] = ~0ull;
         }
@@ -1271,8 +1272,7 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
               const int t = t0 + j * NT;
               if (t < nq) {
                 const int e = sb0 + t / Q, f = t - (t / Q) * Q;
-                const size_t li = (unsigned)keys[e];
-                v[j] = __ldcg(reinterpret_cast<const float4*>(p.list_vals + li * d) + f);
+                v[j] = __ldcg(reinterpret_cast<const float4*>(ls.val((unsigned)keys[e], d)) + f);
               }
             }
             #pragma unroll
@@ -1283,8 +1283,7 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
           #pragma unroll 1
           for (int t = tid; t < (sb1 - sb0) * d; t += NT) {
             const int e = sb0 + t / d, f = t % d;
-            const size_t li = (unsigned)keys[e];
-            stage[t] = __ldcg(p.list_vals + li * d + f);
+            stage[t] = __ldcg(ls.val((unsigned)keys[e], d) + f);
           }
         }
         __syncthreads();
@@ -1343,10 +1342,20 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
         if (sb0 / lay.SB < 4) trace_mark(p, 51 + 2 * (sb0 / lay.SB));
         // C += -lr * total for the segments that end in this window, with
         // several row reads in flight per thread (not one dependent global
-        // round trip per (segment, column))
+        // round trip per (segment, column)); or emit (row, total)
         {
           const int fin0 = (nsw > 0 && seg[she] > sb1) ? she - 1 : she;   // segments [slo, fin0) end here
           const int nfin = fin0 - slo;
+          if (emit_rows) {
+            #pragma unroll 1
+            for (int t = tid; t < nfin * d; t += NT) {
+              const int sidx = slo + t / d, f = t - (t / d) * d;
+              const int a0 = max(seg[sidx], sb0);
+              if (f == 0) emit_rows[emitted + sidx - slo] = (int)(keys[seg[sidx]] >> 32);
+              emit_vals[(size_t)(emitted + sidx - slo) * d + f] = stage[(size_t)(a0 - sb0) * d + f];
+            }
+            emitted += nfin;
+          } else {
           const bool v4 = (d & 3) == 0;
           const int W4 = v4 ? d >> 2 : d;
           #pragma unroll 1
@@ -1383,6 +1392,7 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
                 *reinterpret_cast<float*>(dst[j]) = cur[j].x + nlr * tot[j].x;
             }
           }
+          }
         }
         __syncthreads();
         if (sb0 == 0) trace_mark(p, 45);
@@ -1392,18 +1402,21 @@ __device__ void scatter_det_sorted(const StepParams& p, unsigned char* sm) {
     La = Lb;
   }
   trace_mark(p, 43);
+  return emitted;
 }
 
 // Trip 1 of the owner merge: CTA q's entry count in every list, scanned into
 // lbase (entry base per list) and loff (offset of q's bucket inside the list).
-// Returns M, the owner's entry count.
-__device__ int det_counts(const StepParams& p, unsigned char* sm, int pre_a, int pre_b) {
+// Returns M, the owner's entry count; *base_q (if given) receives the sum of
+// loff over the lists = the entries of owners < q, where owner q's merged rows
+// start in a data-parallel record (so the record layout is deterministic).
+__device__ int det_counts(const StepParams& p, unsigned char* sm, int pre_a, int pre_b, int* base_q = nullptr) {
   const Layout& lay = p.lay;
-  const int tid = threadIdx.x, NT = blockDim.x, q = blockIdx.x, P = p.P, NL = p.NLtot;
+  const int tid = threadIdx.x, NT = blockDim.x, q = blockIdx.x, P = p.P, NL = p.NL;
   int* lbase = reinterpret_cast<int*>(sm + lay.lbase);
   int* loff = reinterpret_cast<int*>(sm + lay.loff);
   int* ws = reinterpret_cast<int*>(sm + lay.ws2);
-  int running = 0;
+  int running = 0, asum = 0;
   #pragma unroll 1
   for (int L0 = 0; L0 < NL; L0 += NT) {
     const int L = L0 + tid;
@@ -1416,6 +1429,7 @@ __device__ int det_counts(const StepParams& p, unsigned char* sm, int pre_a, int
         b = __ldcg(off + q + 1);
       }
       loff[L] = a;
+      asum += a;
       cnt = b - a;
     }
     int tot;
@@ -1423,6 +1437,7 @@ __device__ int det_counts(const StepParams& p, unsigned char* sm, int pre_a, int
     if (L < NL) lbase[L] = running + ex;
     running += tot;
   }
+  if (base_q) block_excl_scan(asum, ws, base_q);
   if (tid == 0) lbase[NL] = running;
   __syncthreads();
   return running;
@@ -1445,41 +1460,39 @@ __device__ void phase2_prep(const StepParams& p, unsigned char* sm) {
 
 // Issue half: entry sources, then trip 2 (row ids, then the gradient partials)
 // as cp.async groups -- returns at once so the dense update runs while they are
-// in flight.
-__device__ void det_issue(const StepParams& p, unsigned char* sm, int M) {
+// in flight.  NL lists described by lbase / loff (smem) and `ls`.
+__device__ void det_issue(const StepParams& p, unsigned char* sm, int M, int NL, const Lists& ls) {
   const Layout& lay = p.lay;
   const int tid = threadIdx.x, NT = blockDim.x;
-  const int d = p.d, NL = p.NLtot;
+  const int d = p.d;
   const int* lbase = reinterpret_cast<const int*>(sm + lay.lbase);
   const int* loff = reinterpret_cast<const int*>(sm + lay.loff);
-  int* esrc = reinterpret_cast<int*>(sm + lay.esrc);
+  unsigned* esrc = reinterpret_cast<unsigned*>(sm + lay.esrc);
   int* erow = reinterpret_cast<int*>(sm + lay.erow);
-  int* hkey = reinterpret_cast<int*>(sm + lay.hkey);
-  int* hfirst = reinterpret_cast<int*>(sm + lay.hfirst);
   float* stage = reinterpret_cast<float*>(sm + lay.stage);
   #pragma unroll 1
   for (int L = tid; L < NL; L += NT) {   // entries of list L: [lbase[L], lbase[L+1])
     const int b = lbase[L], cnt = lbase[L + 1] - b;
     #pragma unroll 1
-    for (int j = 0; j < cnt; ++j) esrc[b + j] = (int)list_index(p, L, loff[L] + j);
+    for (int j = 0; j < cnt; ++j) esrc[b + j] = ls.code(L, loff[L] + j);
   }
   __syncthreads();
   trace_mark(p, 20);
   #pragma unroll 1
-  for (int e = tid; e < M; e += NT) cp_async4(erow + e, p.list_rows + esrc[e]);
+  for (int e = tid; e < M; e += NT) cp_async4(erow + e, ls.row(esrc[e]));
   asm volatile("cp.async.commit_group;" ::: "memory");
   if ((d & 3) == 0) {
     const int Q = d >> 2;
     #pragma unroll 2
     for (int it = tid; it < M * Q; it += NT) {
       const int e = it / Q, q = it - e * Q;
-      cp_async16(stage + (size_t)e * d + 4 * q, p.list_vals + (size_t)esrc[e] * d + 4 * q);
+      cp_async16(stage + (size_t)e * d + 4 * q, ls.val(esrc[e], d) + 4 * q);
     }
   } else {
     #pragma unroll 1
     for (int t = tid; t < M * d; t += NT) {
       const int e = t / d, f = t - e * d;
-      cp_async4(stage + t, p.list_vals + (size_t)esrc[e] * d + f);
+      cp_async4(stage + t, ls.val(esrc[e], d) + f);
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -1488,9 +1501,11 @@ __device__ void det_issue(const StepParams& p, unsigned char* sm, int M) {
 // Deterministic owner merge (hash fast path, M <= MCAP): CTA q owns rows with
 // row % P == q.  Its entries are staged in (list, position) order -- list
 // order is the fixed summation order -- and each distinct row's partials are
-// summed in that order, then C[row] += -lr * sum (one rounding).  Runs after
-// det_issue.
-__device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool write) {
+// summed in that order, then C[row] += -lr * sum (one rounding), or, with
+// emit_rows, the (row, sum) pairs are written to emit_rows / emit_vals
+// [0, nrows) (a data-parallel record).  Runs after det_issue; returns nrows.
+__device__ int det_merge(const StepParams& p, unsigned char* sm, int M, bool write, int32_t* emit_rows = nullptr,
+                         float* emit_vals = nullptr) {
   const Layout& lay = p.lay;
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
   const int d = p.d;
@@ -1547,7 +1562,7 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
   // they fit (rows beyond the stage capacity are read directly when applied)
   const int Q = d >> 2;
   const bool quad = (d & 3) == 0;
-  const int ccap = quad ? min(nrows, lay.MCAP - M) : 0;
+  const int ccap = (quad && !emit_rows) ? min(nrows, lay.MCAP - M) : 0;
   #pragma unroll 2
   for (int it = tid; it < ccap * Q; it += NT) {
     const int ri = it / Q, q = it - ri * Q;
@@ -1585,12 +1600,14 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
   }
   // long rows (more than kLongRow partials: the Zipf head rows this CTA owns) are
   // summed in kLongRow-entry segments by separate threads, then the segments are
-  // added in order -- a fixed association that depends only on the row's count
+  // added in order -- a fixed association that depends only on the row's count.
+  // lpart holds the worst case (Layout::NSEG), so EVERY long row splits; the
+  // atomicAdd only decides where a row's segments are stored, not the sums.
   constexpr int kLongRow = 32;
   int* rsplit = rcur;                                   // row -> first segment, -1: not split
-  int* segrow = hrid;                                   // segment -> row (-1: unused)
-  float4* lpart = reinterpret_cast<float4*>(hkey);      // [segment][Q] partial sums (hkey|hfirst)
-  const int maxseg = quad ? (2 * HS * 4) / (Q * 16) : 0;
+  int* segrow = hrid;                                   // segment -> row
+  float4* lpart = reinterpret_cast<float4*>(sm + lay.lpart);   // [segment][Q] partial sums
+  const int maxseg = quad ? lay.NSEG : 0;
   int* segidx = hrid + maxseg;
   #pragma unroll 1
   for (int r = tid; r < nrows; r += NT) {
@@ -1598,17 +1615,15 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
     const int m = rcnt[r];
     if (quad && m > kLongRow) {
       const int S = (m + kLongRow - 1) / kLongRow;
-      b = atomicAdd(&s_nseg, S);
-      const bool fits = b + S <= maxseg;
-      for (int t = 0; t < S && b + t < maxseg; ++t) { segrow[b + t] = fits ? r : -1; segidx[b + t] = t; }
-      if (!fits) b = -1;
+      b = atomicAdd(&s_nseg, S);   // b + S <= NSEG by construction (sum of S over long rows)
+      for (int t = 0; t < S; ++t) { segrow[b + t] = r; segidx[b + t] = t; }
     }
     rsplit[r] = b;
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   trace_mark(p, 24);
-  const int nseg = s_nseg < maxseg ? s_nseg : maxseg;
+  const int nseg = s_nseg;
   // ---- ordered sum of each distinct row's partials, one RMW of C; one thread
   // per (row, feature quad) when d % 4 == 0, else one warp per row
   if (quad) {
@@ -1627,7 +1642,10 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
       const int ri = k - nseg;
       if (rsplit[ri] >= 0) continue;
       const float4 a = ordered_quadsum(S4, hlist + roff[ri], rcnt[ri], Q, q);
-      if (write) {
+      if (emit_rows) {
+        if (q == 0) emit_rows[ri] = rrow[ri];
+        reinterpret_cast<float4*>(emit_vals + (size_t)ri * d)[q] = a;
+      } else if (write) {
         float4* c4 = reinterpret_cast<float4*>(p.C + (size_t)rrow[ri] * d) + q;
         const float4 o = ri < ccap ? S4[(size_t)(M + ri) * Q + q] : __ldcg(c4);
         *c4 = make_float4(o.x + nlr * a.x, o.y + nlr * a.y, o.z + nlr * a.z, o.w + nlr * a.w);
@@ -1646,7 +1664,10 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
           const float4 v = lpart[(k + t) * Q + q];
           a = make_float4(a.x + v.x, a.y + v.y, a.z + v.z, a.w + v.w);
         }
-        if (write) {
+        if (emit_rows) {
+          if (q == 0) emit_rows[r] = rrow[r];
+          reinterpret_cast<float4*>(emit_vals + (size_t)r * d)[q] = a;
+        } else if (write) {
           float4* c4 = reinterpret_cast<float4*>(p.C + (size_t)rrow[r] * d) + q;
           const float4 o = r < ccap ? S4[(size_t)(M + r) * Q + q] : __ldcg(c4);
           *c4 = make_float4(o.x + nlr * a.x, o.y + nlr * a.y, o.z + nlr * a.z, o.w + nlr * a.w);
@@ -1663,7 +1684,14 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
       for (int f0 = 0; f0 < d; f0 += 128) {
         const float4 a4 = ordered_rowsum(stage, ps, nm, d, f0);
         const float acc[4] = {a4.x, a4.y, a4.z, a4.w};
-        if (write) {
+        if (emit_rows) {
+          if (lane == 0 && f0 == 0) emit_rows[ri] = rrow[ri];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int f = f0 + lane + 32 * k;
+            if (f < d) emit_vals[(size_t)ri * d + f] = acc[k];
+          }
+        } else if (write) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const int f = f0 + lane + 32 * k;
@@ -1674,6 +1702,7 @@ __device__ void det_merge(const StepParams& p, unsigned char* sm, int M, bool wr
     }
   }
   __syncthreads();
+  return nrows;
 }
 
 // Atomic scatter: CTA b applies lists L = b, b+G, ... with red.global.add.v4.f32.
@@ -1682,12 +1711,12 @@ __device__ void phase2_scatter_atomic(const StepParams& p) {
   const int P = p.P, d = p.d;
   const float nlr = -p.lr;
   #pragma unroll 1
-  for (int L = blockIdx.x; L < p.NLtot; L += gridDim.x) {
+  for (int L = blockIdx.x; L < p.NL; L += gridDim.x) {
     const int U0 = __ldcg(p.list_off + (size_t)L * (P + 1));
     const int U1 = __ldcg(p.list_off + (size_t)L * (P + 1) + P);
     #pragma unroll 1
     for (int j = U0 + warp; j < U1; j += NW) {
-      const size_t ix = list_index(p, L, j);
+      const size_t ix = (size_t)L * p.cap + j;
       const int row = __ldcg(p.list_rows + ix);
       const float* src = p.list_vals + ix * d;
       float* dst = p.C + (size_t)row * d;
@@ -1727,13 +1756,13 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
       const int r = lane + 32 * k;
-      hv[k] = r < p.Ptot ? __ldcg(reinterpret_cast<const float2*>(p.dense_part + (size_t)r * p.dense_stride + hoff))
+      hv[k] = r < p.P ? __ldcg(reinterpret_cast<const float2*>(p.dense_part + (size_t)r * p.dense_stride + hoff))
                          : make_float2(0.f, 0.f);
     }
   }
   // owner counts for lists [0, NT)
   int pre_a = 0, pre_b = 0;
-  if (p.mode == 0 && tid < p.NLtot) {
+  if (p.mode == 0 && tid < p.NL) {
     const int32_t* off = p.list_off + (size_t)tid * (p.P + 1) + blockIdx.x;
     pre_a = __ldcg(off);
     pre_b = __ldcg(off + 1);
@@ -1757,23 +1786,13 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
     unsigned fl = 0;
 #pragma unroll
     for (int k = 0; k < 5; ++k) { acc += hv[k].x; fl |= (unsigned)__float_as_int(hv[k].y); }
-    #pragma unroll 1
-    for (int r0 = 160; r0 < p.Ptot; r0 += 32) {   // only with many ranks
-      const int r = r0 + lane;
-      const float2 v = r < p.Ptot ? __ldcg(reinterpret_cast<const float2*>(p.dense_part + (size_t)r * p.dense_stride + hoff))
-                                  : make_float2(0.f, 0.f);
-      acc += v.x;
-      fl |= (unsigned)__float_as_int(v.y);
-    }
     acc = warp_sum(acc);
     fl = __reduce_or_sync(0xffffffffu, fl);
-    if (lane == 0) {
-      s_loss = acc * p.inv_B;
-      if (p.flags_from_records) s_flags = (int)fl;   // data parallel: every rank skips together
-    }
+    if (lane == 0) s_loss = acc * p.inv_B;
+    (void)fl;
   }
   if (tid == 0) {
-    if (!p.flags_from_records) s_flags = f0;
+    s_flags = f0;
     if (blockIdx.x == 0) st->last_bad = bad;
   }
   trace_mark(p, 29);
@@ -1799,7 +1818,8 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
   }
   trace_mark(p, 8);
   const bool hashed = p.mode == 0 && M > 0 && M <= p.lay.MCAP;
-  if (hashed) det_issue(p, sm, M);   // trip 2 in flight during the dense update
+  const Lists ls{p.list_rows, p.list_vals, p.cap, 0};
+  if (hashed) det_issue(p, sm, M, p.NL, ls);   // trip 2 in flight during the dense update
   // ---- dense update (first block prefetched; further blocks only when P is small)
   if (nq0 > 0) dense_apply(p, sm, ds.q0, nq0, groups0, dacc0, make_float4(cur0[0], cur0[1], cur0[2], cur0[3]), write);
   #pragma unroll 1
@@ -1819,7 +1839,7 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
   // ---- embedding scatter-add
   if (p.mode == 0) {
     if (hashed) det_merge(p, sm, M, write);
-    else if (M > 0 && write) scatter_det_sorted(p, sm);
+    else if (M > 0 && write) scatter_det_sorted(p, sm, ls);
   } else if (write) {
     phase2_scatter_atomic(p);
   }
@@ -1830,64 +1850,298 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
   }
 }
 
-// ------------------------------------------------------------------ data-parallel record
-// After phase 1 (and the in-rank grid barrier): this rank's compact record for
-// the all-gather -- the dense partials summed in CTA order, the hinge sum and
-// flags, and every list's entries compacted into one array with absolute
-// per-owner offsets.
-__device__ void build_record(const StepParams& p, unsigned char* sm) {
-  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
-  const int P = p.P, d = p.d, NL = p.NLtot;
-  int* ws = reinterpret_cast<int*>(sm + p.lay.ws2);
-  // dense sums: this CTA's quad slice over the P partials
+// ------------------------------------------------------------------ data parallel
+// One synchronous DP step (PAPER.md:219-220 names distributed
+// gradient descent as the next step).  Every rank runs phase 1 on its shard,
+// then (publish) each owner CTA q merges the rows it owns over the rank's own
+// lists -- one (row, gradient-sum) entry per distinct row, the "per-rank
+// dedup" -- and writes them, with its slice of the rank's dense-gradient sum,
+// the rank's hinge sum and error flags, into the rank's exchange window.
+// (merge) CTA q of every rank then reads owner q's entries and dense slice of
+// all G ranks, sums each row's and each dense element's G partials in rank
+// order and applies the update.  Identical inputs in an identical order on
+// every rank: replicas stay bit-identical, and the result does not depend on
+// how the records travelled (peer loads over NVLink, an NCCL all-gather, or
+// device copies between replicas of one GPU).
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// The rank's hinge sum over its P partial records (fixed association: lane-
+// strided sums, then a butterfly) -- every CTA computes the same value.
+__device__ __forceinline__ float rank_hinge(const StepParams& p) {
+  const int lane = threadIdx.x & 31;
+  float acc = 0.f;
+  #pragma unroll 1
+  for (int r = lane; r < p.P; r += 32) acc += __ldcg(p.dense_part + (size_t)r * p.dense_stride + p.dense_len);
+  return warp_sum(acc);
+}
+
+__device__ void dp_publish(const StepParams& p, unsigned char* sm) {
+  __shared__ unsigned s_epoch;
+  __shared__ int s_flags;
+  __shared__ float s_hinge;
+  const int tid = threadIdx.x, NT = blockDim.x, warp = tid >> 5, q = blockIdx.x, d = p.d;
+  DevStatus* st = p.st;
+  unsigned my_done = 0;
+  int pre_a = 0, pre_b = 0;
+  if (tid < p.NL) {   // owner counts for lists [0, NT), issued with the other trip-1 reads
+    const int32_t* off = p.list_off + (size_t)tid * (p.P + 1) + q;
+    pre_a = __ldcg(off);
+    pre_b = __ldcg(off + 1);
+  }
+  if (tid == 0) {
+    s_epoch = p.xepoch[q] + 1u;
+    s_flags = __ldcg(&st->flags);
+    if (q == 0) st->last_bad = __ldcg(&st->bad);
+    my_done = atomicAdd(&st->done, 1u);
+  }
+  if (warp == 1) {
+    const float hsum = rank_hinge(p);
+    if ((tid & 31) == 0) s_hinge = hsum;
+  }
+  int base = 0;
+  const int M = det_counts(p, sm, pre_a, pre_b, &base);   // contains __syncthreads
+  const unsigned epoch = s_epoch;
+  const int par = p.xgathered ? 0 : (int)(epoch & 1u);
+  unsigned char* blk = p.xwin + p.xl.blk[par];
+  int32_t* erows = reinterpret_cast<int32_t*>(blk + p.xl.rows) + base;
+  float* evals = reinterpret_cast<float*>(blk + p.xl.vals) + (size_t)base * d;
+  float* dense = reinterpret_cast<float*>(p.xwin + p.xl.dense[par]);
+  const Lists ls{p.list_rows, p.list_vals, p.cap, 0};
+  const bool hashed = M > 0 && M <= p.lay.MCAP;
+  if (hashed) det_issue(p, sm, M, p.NL, ls);   // entries in flight during the dense sums
+  // this CTA's slice of the rank's dense-gradient sum (P records, record order)
   const DenseSlice ds = dense_slice(p);
-#pragma unroll 1
+  #pragma unroll 1
   for (int qb = ds.q0; qb < ds.q1; qb += NT) {
     const int nq = min(NT, ds.q1 - qb), groups = dense_groups(nq, NT);
     dense_apply(p, sm, qb, nq, groups, dense_partial(p, qb, nq, groups), make_float4(0.f, 0.f, 0.f, 0.f), false,
-                p.send_dense);
+                dense);
   }
-  if (blockIdx.x == 0 && warp == 0) {
-    float acc = 0.f;
-    for (int r = lane; r < P; r += 32) acc += __ldcg(p.dense_part + (size_t)r * p.dense_stride + p.dense_len);
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      p.send_dense[p.dense_len] = acc;
-      p.send_dense[p.dense_len + 1] = __int_as_float(__ldcg(&p.st->flags));
+  if (q == 0 && tid == 0) {   // hinge | flags words (summed by the NCCL all-reduce exchanges)
+    dense[p.dense_len] = s_hinge;
+    dense[p.dense_len + 1] = s_flags ? 1.f : 0.f;
+  }
+  int count = 0;
+  if (hashed) count = det_merge(p, sm, M, true, erows, evals);
+  else if (M > 0) count = scatter_det_sorted(p, sm, ls, erows, evals);
+  if (tid == 0) {
+    XHdr* hdr = reinterpret_cast<XHdr*>(blk) + q;
+    *hdr = XHdr{s_flags, s_hinge, base, count};
+  }
+  __syncthreads();
+  if (tid == 0) {
+    p.xepoch[q] = epoch;
+    if (p.xpeer) {   // this CTA's part of the record is complete: tell every rank
+      __threadfence_system();
+      #pragma unroll 1
+      for (int r = 0; r < p.world; ++r) {
+        unsigned* f = reinterpret_cast<unsigned*>(const_cast<unsigned char*>(p.xbase) + (size_t)r * p.xstride + p.xl.flags);
+        st_release_sys(f + (size_t)p.rank * kMaxSMs + q, epoch);
+      }
+    }
+    if (my_done == gridDim.x - 1) {   // every CTA has read this step's flags
+      st->flags = 0;
+      st->bad = kNoBad;
+      st->done = 0;
     }
   }
-  // compaction: CTA b copies its lists L = b*R + r to [base_L, base_L + U_L)
-  __shared__ int s_base;
-#pragma unroll 1
-  for (int r = 0; r < p.R; ++r) {
-    const int L = blockIdx.x * p.R + r;
-    int part = 0;
-    for (int l = tid; l < L; l += NT) part += __ldcg(p.list_off + (size_t)l * (P + 1) + P);
-    int base;
-    block_excl_scan(part, ws, &base);   // total over lists < L
-    const int32_t* off = p.list_off + (size_t)L * (P + 1);
-    const int U = __ldcg(off + P);
-    for (int q = tid; q <= P; q += NT) p.send_off[(size_t)L * (P + 1) + q] = base + __ldcg(off + q);
-    const int32_t* lrows = p.list_rows + (size_t)L * p.list_stride;
-    const float* lvals = p.list_vals + (size_t)L * p.list_stride * d;
-    for (int j = tid; j < U; j += NT) p.send_rows[base + j] = __ldcg(lrows + j);
-    for (int t = tid; t < U * d; t += NT) p.send_vals[(size_t)base * d + t] = __ldcg(lvals + t);
-    (void)s_base; (void)NW; (void)NL;
+}
+
+// Merge: owner q of all ranks, rank order.  Needs phase2_prep + a barrier first.
+__device__ void dp_merge(const StepParams& p, unsigned char* sm) {
+  __shared__ int s_flags, s_M;
+  __shared__ float s_loss;
+  __shared__ unsigned s_epoch;
+  const Layout& lay = p.lay;
+  const int tid = threadIdx.x, NT = blockDim.x, q = blockIdx.x, d = p.d, G = p.world;
+  DevStatus* st = p.st;
+  int* lbase = reinterpret_cast<int*>(sm + lay.lbase);
+  int* loff = reinterpret_cast<int*>(sm + lay.loff);
+  if (tid == 0) {
+    const unsigned epoch = p.xepoch[q];
+    s_epoch = epoch;
+    int fl = 0;
+    if (p.xpeer) {   // wait until owner q of every rank has published this step
+      const unsigned* f = reinterpret_cast<const unsigned*>(p.xwin + p.xl.flags) + q;
+      const unsigned long long t0 = globaltimer_ns();
+      #pragma unroll 1
+      for (int r = 0; r < G; ++r) {
+        while ((int)(ld_acquire_sys(f + (size_t)r * kMaxSMs) - epoch) < 0) {
+          if (globaltimer_ns() - t0 > 20000000000ull) { fl |= 4; break; }   // 20 s: a rank is gone
+          __nanosleep(32);
+        }
+      }
+    }
+    s_flags = fl;
+  }
+  __syncthreads();
+  const int par = p.xgathered ? 0 : (int)(s_epoch & 1u);
+  const unsigned char* blk0 = p.xbase + (p.xgathered ? 0 : p.xl.blk[par]);
+  // headers of owner q, every rank, summed in rank order by one thread
+  if (tid == 0) {
+    int fl = s_flags, M = 0;
+    float hinge = 0.f;
+    unsigned long long xb = 0;
+    #pragma unroll 1
+    for (int r = 0; r < G; ++r) {
+      const int4 h = __ldcg(reinterpret_cast<const int4*>(blk0 + (size_t)r * p.xstride) + q);
+      fl |= h.x;
+      hinge += __int_as_float(h.y);
+      loff[r] = h.z;
+      lbase[r] = M;
+      M += h.w;
+      if (r != p.rank) xb += sizeof(XHdr) + (unsigned long long)h.w * (4ull + 4ull * d);
+    }
+    lbase[G] = M;
+    s_M = M;
+    const float loss = hinge * p.inv_B;
+    s_loss = loss;
+    s_flags = fl | (!isfinite(loss) ? 2 : 0);
+    if (p.xstats) {
+      const DenseSlice ds = dense_slice(p);
+      if (!p.xdense) xb += (unsigned long long)(G - 1) * 16ull * (ds.q1 - ds.q0);
+      atomicAdd(p.xstats, xb);
+      atomicMax(p.xstats + 1, (unsigned long long)M);
+    }
+    if (q == 0) {
+      const int flags = s_flags;
+      st->last_loss = loss;
+      st->last_flags = flags;
+      st->rank_flags = flags;
+      if (p.loss_out) *p.loss_out = loss;
+      if (flags) {
+        atomicOr(&st->sticky_flags, flags);
+        atomicMin(&st->sticky_bad, st->last_bad);
+      }
+    }
+  }
+  __syncthreads();
+  const int M = s_M;
+  const bool write = s_flags == 0;
+  const Lists ls{reinterpret_cast<const int32_t*>(blk0 + p.xl.rows), reinterpret_cast<const float*>(blk0 + p.xl.vals), 0,
+                 p.xstride};
+  const bool hashed = M > 0 && M <= lay.MCAP;
+  if (hashed) det_issue(p, sm, M, G, ls);   // entries in flight during the dense update
+  // dense: this CTA's slice, the G ranks' sums added in rank order (or the
+  // NCCL all-reduced vector), then W1 / b1 / w2 -= lr * sum
+  {
+    const DenseSlice ds = dense_slice(p);
+    const int ndh = p.n * p.d * p.h, DL = p.dense_len;
+    #pragma unroll 1
+    for (int qi = ds.q0 + tid; qi < ds.q1; qi += NT) {
+      float4 acc;
+      if (p.xdense) {
+        acc = ldcg4(p.xdense + 4 * qi);
+      } else {
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        const unsigned char* db = p.xbase + p.xl.dense[par];
+        #pragma unroll 1
+        for (int r = 0; r < G; ++r) {
+          const float4 v = ldcg4(reinterpret_cast<const float*>(db + (size_t)r * p.xstride) + 4 * qi);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+      }
+      const float sv[4] = {acc.x, acc.y, acc.z, acc.w};
+      const int base = 4 * qi;
+      if (write) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (base + k >= DL) break;
+          float* ptr = param_ptr(p, base + k, ndh);
+          const float nv = __ldcg(ptr) - p.lr * sv[k];
+          *ptr = nv;
+          if (p.W1T != nullptr && base + k < ndh) {
+            const int row = (base + k) / p.h, u = base + k - row * p.h;
+            p.W1T[(size_t)u * (p.n * p.d) + row] = nv;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (hashed) det_merge(p, sm, M, write);
+  else if (M > 0 && write) scatter_det_sorted(p, sm, ls);
+}
+
+// NCCL table exchange (PG_EXCHANGE_TABLE): this rank's merged rows into the
+// zeroed V x d gradient table (a row is at most in two entries of one owner --
+// sorted-fallback window split -- and two float adds commute exactly).
+__global__ void dp_table_scatter_kernel(StepParams p, float* table) {
+  const unsigned char* blk = p.xwin + p.xl.blk[0];
+  const int q = blockIdx.x, d = p.d;
+  const int4 h = __ldcg(reinterpret_cast<const int4*>(blk) + q);
+  const int32_t* rows = reinterpret_cast<const int32_t*>(blk + p.xl.rows) + h.z;
+  const float* vals = reinterpret_cast<const float*>(blk + p.xl.vals) + (size_t)h.z * d;
+  #pragma unroll 1
+  for (int t = threadIdx.x; t < h.w * d; t += blockDim.x) {
+    const int e = t / d, f = t - e * d;
+    atomicAdd(table + (size_t)rows[e] * d + f, vals[t]);
+  }
+}
+
+// After the all-reduces: W1 / b1 / w2 -= lr * dense, C += -lr * table on every
+// row (adding -lr * 0 leaves a row bit-identical), table re-zeroed; gated on
+// the reduced flags / loss.  xdense = reduced [dense | hinge | flags].
+__global__ void dp_table_apply_kernel(StepParams p, float* table, int zero) {
+  const float hinge = __ldcg(p.xdense + p.dense_len), flagsum = __ldcg(p.xdense + p.dense_len + 1);
+  const float loss = hinge * p.inv_B;
+  const int flags = (flagsum != 0.f ? 1 : 0) | (!isfinite(loss) ? 2 : 0);
+  const bool write = flags == 0;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, NT = (size_t)gridDim.x * blockDim.x;
+  if (tid == 0) {
+    DevStatus* st = p.st;
+    st->last_loss = loss;
+    st->last_flags = flags;
+    st->rank_flags = flags;
+    if (p.loss_out) *p.loss_out = loss;
+    if (flags) {
+      atomicOr(&st->sticky_flags, flags);
+      atomicMin(&st->sticky_bad, st->last_bad);
+    }
+  }
+  const int ndh = p.n * p.d * p.h;
+  if (write)
+    for (size_t i = tid; i < (size_t)p.dense_len; i += NT) {
+      float* ptr = param_ptr(p, (int)i, ndh);
+      const float nv = *ptr - p.lr * __ldcg(p.xdense + i);
+      *ptr = nv;
+      if (p.W1T != nullptr && (int)i < ndh) {
+        const int row = (int)i / p.h, u = (int)i - row * p.h;
+        p.W1T[(size_t)u * (p.n * p.d) + row] = nv;
+      }
+    }
+  const size_t n4 = (size_t)p.V * p.d / 4;
+  const float nlr = -p.lr;
+  float4* T4 = reinterpret_cast<float4*>(table);
+  float4* C4 = reinterpret_cast<float4*>(p.C);
+  for (size_t i = tid; i < n4; i += NT) {
+    const float4 g = T4[i];
+    if (write) {
+      float4 c = C4[i];
+      c.x += nlr * g.x; c.y += nlr * g.y; c.z += nlr * g.z; c.w += nlr * g.w;
+      C4[i] = c;
+    }
+    if (zero) T4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
 // ------------------------------------------------------------------ kernels
-template <int PATH>   // 0 generic, 1 fast (h == 32), 2/3/4 tiled with 16/4/8-example chunks
+template <int PATH, int DP>   // PATH: 0 generic, 1 fast (h == 32), 2/3/4 tiled with 16/4/8-example chunks
 __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) {
   extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + p.lay.mbar);
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_init(&bars[2], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
   trace_mark(p, 0);
   trace_clock(p, 12);
   if (phases & 1) {
@@ -1899,8 +2153,8 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
     __syncthreads();
     trace_mark(p, 6);
   }
-  const bool prep = (phases & 2) && p.mode == 0;
-  if ((phases & 1) && (phases & 6)) {
+  const bool prep = DP ? (phases & 8) != 0 : ((phases & 2) && p.mode == 0);
+  if ((phases & 1) && (phases & 10)) {
     const unsigned long long target = grid_arrive(&p.st->bar_arrivals[gridDim.x - 1]);
     if (prep) phase2_prep(p, smem);   // overlaps the barrier
     grid_wait(&p.st->bar_arrivals[gridDim.x - 1], target);
@@ -1909,8 +2163,16 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) 
     __syncthreads();
   }
   trace_mark(p, 7);
-  if (phases & 4) build_record(p, smem);
-  if (phases & 2) phase2(p, smem);
+  if (DP) {
+    if (phases & 8) dp_publish(p, smem);
+    if (phases & 16) {
+      phase2_prep(p, smem);
+      __syncthreads();
+      dp_merge(p, smem);
+    }
+  } else if (phases & 2) {
+    phase2(p, smem);
+  }
   __syncthreads();
   trace_mark(p, 11);
   trace_clock(p, 13);
@@ -1942,57 +2204,60 @@ int step_chunk_T(int d, int n, int h, int fast, int per_cta) {
 }
 
 // The tiled path has one kernel per chunk size, so neither carries the other's
-// code (a combined kernel ran the 16-example case 12 % slower).
-static const void* step_fn(int fast, int T) {
+// code (a combined kernel ran the 16-example case 12 % slower); the data-
+// parallel phases live in their own instantiations (DP = 1), so the one-GPU
+// kernel carries none of their code either.
+template <int DP>
+static const void* step_fn_t(int fast, int T) {
   if (fast == 2)
-    return T == kTTSmall ? (const void*)step_kernel<3> : T == kTTMid ? (const void*)step_kernel<4> : (const void*)step_kernel<2>;
-  return fast == 1 ? (const void*)step_kernel<1> : (const void*)step_kernel<0>;
+    return T == kTTSmall ? (const void*)step_kernel<3, DP>
+           : T == kTTMid ? (const void*)step_kernel<4, DP>
+                         : (const void*)step_kernel<2, DP>;
+  return fast == 1 ? (const void*)step_kernel<1, DP> : (const void*)step_kernel<0, DP>;
 }
+static const void* step_fn(int fast, int T, int dp) { return dp ? step_fn_t<1>(fast, T) : step_fn_t<0>(fast, T); }
 
 // Allow up to the opt-in maximum minus the kernel's static shared memory.
 cudaError_t step_prepare(int fast, size_t optin, size_t* usable) {
   size_t best = optin;
-  for (int T : {kTT, kTTSmall, kTTMid}) {
-    const void* fn = step_fn(fast, T);
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
-    if (e != cudaSuccess) return e;
-    const size_t smem = optin - fa.sharedSizeBytes;
-    if (smem < best) best = smem;
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    if (fast != 2) break;
-  }
+  for (int dp = 0; dp < 2; ++dp)
+    for (int T : {kTT, kTTSmall, kTTMid}) {
+      const void* fn = step_fn(fast, T, dp);
+      cudaFuncAttributes fa;
+      cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+      if (e != cudaSuccess) return e;
+      const size_t smem = optin - fa.sharedSizeBytes;
+      if (smem < best) best = smem;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      if (fast != 2) break;
+    }
   if (usable) *usable = best;
   return cudaSuccess;
 }
 
 void launch_step_phases(const StepParams& p, int phases, int fast, cudaStream_t s, int* launches) {
   const int NT = step_block_threads(p.d, p.n, p.h, fast);
-  const void* fn = step_fn(fast, p.T);
+  const void* fn = step_fn(fast, p.T, (phases & 24) != 0);
   void* args[] = {(void*)&p, (void*)&phases};
-  if ((phases & 1) && (phases & 6)) cudaLaunchCooperativeKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
+  if ((phases & 1) && (phases & 10)) cudaLaunchCooperativeKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
   else cudaLaunchKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
   *launches += 1;
 }
 
 void launch_step(const StepParams& p, int fused, int fast, cudaStream_t s, int* launches) {
-  const int NT = step_block_threads(p.d, p.n, p.h, fast);
-  const size_t smem = (size_t)p.smem_bytes;
-  const void* fn = step_fn(fast, p.T);
   if (fused) {
-    int phases = 3;
-    void* args[] = {(void*)&p, (void*)&phases};
-    cudaLaunchCooperativeKernel(fn, dim3(p.P), dim3(NT), args, smem, s);
-    *launches += 1;
+    launch_step_phases(p, 3, fast, s, launches);
   } else {
-    int ph1 = 1, ph2 = 2;
-    void* a1[] = {(void*)&p, (void*)&ph1};
-    void* a2[] = {(void*)&p, (void*)&ph2};
-    cudaLaunchKernel(fn, dim3(p.P), dim3(NT), a1, smem, s);
-    cudaLaunchKernel(fn, dim3(p.P), dim3(NT), a2, smem, s);
-    *launches += 2;
+    launch_step_phases(p, 1, fast, s, launches);
+    launch_step_phases(p, 2, fast, s, launches);
   }
+}
+
+void launch_dp_table(const StepParams& p, float* table, int what, int num_sms, cudaStream_t s, int* launches) {
+  if (what) dp_table_apply_kernel<<<num_sms * 4, 256, 0, s>>>(p, table, what == 2);
+  else dp_table_scatter_kernel<<<p.P, 256, 0, s>>>(p, table);
+  *launches += 1;
 }
 
 }  // namespace pg

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "common.cuh"
+
 namespace pg {
 
 constexpr int kTMax = 32;       // examples per chunk
@@ -42,13 +44,15 @@ static_assert(sizeof(DevStatus) == 3 * 128 + 160 * 8, "DevStatus layout");
 // Shared-memory carve-up (byte offsets), computed once on the host.
 struct Layout {
   // phase 1
-  int xs, pg, sig, gz, hinge, rows, ws, red, wsm, mbar;
+  int xs, pg, sig, gz, hinge, rows, ws, red, wsm;
   int ahk, ahc, aslot, ocnt, ocur, hj, ecnt, eoff, ecur, spos, misc, amask, pu, urow, uslot;   // chunk aggregation
   int A, Ac, SIG, DEL, DELc;   // generic path
   int xt, sigu, sige, dwt;      // tiled path
   // phase 2
   int lbase, loff, keys, seg, stage, stagefb, carry, dred, ws2;
   int esrc, erow, hkey, hfirst, heads, hlist, rcnt, roff, rcur, misc2, rmask;
+  int lpart;     // long-row segment partials [NSEG][d] (owner merge)
+  int NSEG;      // worst-case segment count: every long row always splits
   int SB;        // staged rows per sub-batch (sorted fallback)
   int MCAP;      // owner entries handled by the hash fast path
   int HS;        // hash slots (power of two >= 2*MCAP)
@@ -59,7 +63,6 @@ __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
 __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT, int NLtot, int fast) {
   Layout L{};
-  L.mbar = 0;   // three mbarriers (phase-1 gathers, phase-2 staging, C prefetch), never aliased
   int o = 32;
   const int NW = NT / 32;
   if (fast == 1) {
@@ -134,6 +137,11 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.hfirst = o; o = align16(o + HS * 4);
   L.stage = o;  o = align16(o + MCAP * d * 4);
   L.rmask = o;  o = align16(o + MCAP * (512 / 32) * 4);   // per distinct row: member entries
+  // long rows (> 32 entries) are summed in 32-entry segments: at most
+  // ceil(MCAP/32) full segments plus one partial segment per long row, so the
+  // split decision never depends on which row claimed capacity first
+  L.NSEG = (MCAP + 31) / 32 + MCAP / 33 + 1;
+  L.lpart = o;  o = align16(o + L.NSEG * d * 4);
   const int fast_end = o;
   // sorted fallback (aliases the hash path)
   o = p2fixed;
@@ -148,6 +156,53 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.total2 = o > fast_end ? o : fast_end;
   return L;
 }
+
+// Data-parallel exchange window of one rank (byte offsets; SURVEY.md §8(e),
+// §8(f) NEXT-4).  Each rank publishes, per owner CTA q, the rows it owns
+// (row % P == q) merged over its own lists -- one (row, gradient-sum) entry per
+// distinct row -- plus its dense-gradient sum, hinge sum and error flags; the
+// ranks' owner-q CTAs then merge the G records in rank order.
+constexpr int kMaxRanks = 64;
+constexpr unsigned kOffBits = 26;                 // ranked entry code: rank << 26 | offset
+constexpr unsigned kOffMask = (1u << kOffBits) - 1u;
+struct XHdr {
+  int flags;     // the rank's error flags (bit0 bad index)
+  float hinge;   // the rank's hinge sum (record order)
+  int base;      // first entry of owner q in the rank's rows/vals
+  int count;     // entries of owner q
+};
+struct XLayout {
+  size_t flags;      // [kMaxRanks][kMaxSMs] u32: step epoch at which rank r's CTA q published
+  size_t blk[2];     // per parity: [hdr kMaxSMs x XHdr | rows cap | vals cap x d]
+  size_t blk_bytes;
+  size_t rows, vals; // offsets inside a block
+  size_t dense[2];   // per parity: the rank's dense-gradient sum [dense_stride]
+  size_t total;
+};
+
+// Where the (row, gradient) entries of a list live.  Local lists (one GPU,
+// the per-chunk lists of phase 1): entry code L * list_stride + off.  Ranked
+// records (data-parallel merge): list L is rank L's owner-q region, code
+// (L << kOffBits) | off, rank L's arrays xstride bytes after rank L-1's.
+struct Lists {
+  const int32_t* rows;
+  const float* vals;
+  int list_stride;
+  size_t xstride;   // 0: local lists
+  __device__ __forceinline__ unsigned code(int L, int off) const {
+    return xstride ? ((unsigned)L << kOffBits) | (unsigned)off : (unsigned)(L * list_stride + off);
+  }
+  __device__ __forceinline__ const int32_t* row(unsigned c) const {
+    return xstride ? reinterpret_cast<const int32_t*>(reinterpret_cast<const char*>(rows) + (size_t)(c >> kOffBits) * xstride) +
+                         (c & kOffMask)
+                   : rows + c;
+  }
+  __device__ __forceinline__ const float* val(unsigned c, int d) const {
+    return xstride ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(vals) + (size_t)(c >> kOffBits) * xstride) +
+                         (size_t)(c & kOffMask) * d
+                   : vals + (size_t)c * d;
+  }
+};
 
 // Fixed per-step decomposition: P CTAs, CTA p
 // owns examples [p*B/P, (p+1)*B/P), processed in R chunks of <= T examples.
@@ -166,45 +221,47 @@ struct StepParams {
   const int32_t* idx;
   const int32_t* corr;
   int B;
-  float inv_B;   // 1 / global batch
+  float inv_B;   // 1 / global batch (or 1: summed loss)
   int act;       // 0 hardtanh, 1 tanh (PG_OPT_ACTIVATION)
   float lr;
   // decomposition
   int P, R, T, cap;     // cap = (n+1)*T list capacity
   // workspace: per-CTA dense partial records
-  float* dense_part;    // [Ptot][dense_stride]: dW1 | db1 | dw2 | hinge
+  float* dense_part;    // [P][dense_stride]: dW1 | db1 | dw2 | hinge | flags
   int dense_len;        // n*d*h + 2h
-  int dense_stride;     // multiple of 4, > dense_len
+  int dense_stride;     // multiple of 4, > dense_len + 1
   // per-chunk aggregated (row, gradient-sum) lists, bucketed by owner CTA
-  int32_t* list_rows;   // [NLtot][cap]
-  float* list_vals;     // [NLtot][cap][d]
-  int32_t* list_off;    // [NLtot][P+1]  (owner q's entries: [off[q], off[q+1]))
-  // phase 2 sees Ptot records / NLtot lists (== P / P*R on one GPU;
-  // world*P / world*P*R after a data-parallel all-gather)
-  int Ptot, NLtot;
-  // list addressing: entry `off` of list L lives at index
-  //   (L / LPR) * rank_stride + (L % LPR) * list_stride + off
-  // single GPU: LPR = NLtot, list_stride = cap; after a data-parallel gather
-  // of compacted per-rank lists: LPR = lists per rank, list_stride = 0,
-  // rank_stride = entries per rank record (offsets are absolute in the record)
-  int LPR, list_stride, rank_stride;
-  int flags_from_records;   // phase 2 ORs the ranks' flags (dense record word dense_len+1)
-  // data-parallel record build (phase bit 4): this rank's compact record
-  float* send_dense;    // [dense_stride]: dense sums | hinge | flags
-  int32_t* send_off;    // [NL][P+1] absolute offsets into send_rows
-  int32_t* send_rows;   // [rec_cap]
-  float* send_vals;     // [rec_cap][d]
+  int32_t* list_rows;   // [NL][cap]
+  float* list_vals;     // [NL][cap][d]
+  int32_t* list_off;    // [NL][P+1]  (owner q's entries: [off[q], off[q+1]))
+  int NL;               // P * R
   DevStatus* st;
   float* loss_out;      // optional device pointer
   int mode;             // 0 det, 1 atomic
   int smem_bytes;       // dynamic smem requested
-  unsigned long long* trace;  // optional [P][16] %globaltimer stamps (PG_OPT_TRACE)
+  unsigned long long* trace;  // optional [P][64] %globaltimer stamps (PG_OPT_TRACE)
+  // ---- data parallel (phase bits 8: publish, 16: merge)
+  int world, rank;
+  unsigned char* xwin;        // this rank's exchange window
+  const unsigned char* xbase; // rank 0's window (or gathered block) as addressed by this rank
+  size_t xstride;             // bytes from rank r's window (block) to rank r + 1's
+  XLayout xl;
+  int xcap;                   // entries per rank record, (n+1)*B
+  int xpeer;                  // 1: publish pushes ready epochs to every rank's window, merge waits
+  int xgathered;              // 1: records were all-gathered into xbase (parity 0, blocks back to back)
+  unsigned* xepoch;           // [P] per-CTA step counters (this rank)
+  const float* xdense;        // all-reduced dense vector | hinge | flags (NCCL exchanges), else null
+  unsigned long long* xstats; // [0] bytes read from other ranks' records, [1] max entries merged by one owner
   Layout lay;
 };
 
 void launch_step(const StepParams& p, int fused, int fast, cudaStream_t s, int* launches);
-// phases: 1 phase 1, 2 phase 2, 4 data-parallel record (1|4 and 1|2 add the grid barrier)
+// phases: 1 phase 1, 2 phase 2 (one GPU), 8 data-parallel publish, 16 data-
+// parallel merge; 1 together with 2 or 8 adds the in-rank grid barrier
 void launch_step_phases(const StepParams& p, int phases, int fast, cudaStream_t s, int* launches);
+// NCCL table exchange: what = 0 scatter this rank's merged rows into `table`,
+// 1 apply the reduced table and dense vector, 2 apply and re-zero the table
+void launch_dp_table(const StepParams& p, float* table, int what, int num_sms, cudaStream_t s, int* launches);
 int step_fast_ok(int d, int n, int h);
 int step_block_threads(int d, int n, int h, int fast);
 int step_chunk_T(int d, int n, int h, int fast, int per_cta);   // per_cta = ceil(B / P)

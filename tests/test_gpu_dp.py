@@ -1,7 +1,15 @@
-"""Data-parallel step on one B200: G replicas exchange their
-compact records by device copies (pg_train_step_group) -- the same device code
-as the NCCL path except the transport.  Checked against the oracle's G-rank
-emulation (oracle.train_step_dp) and for bit-identical replicas."""
+"""Data-parallel step on one B200.
+
+* pg_train_step_group: G replicas on one device run the kernels of the NCCL
+  path (phase 1 + publish of per-rank merged records, then the rank-order
+  merge), the exchange emulated on the device -- PEER reads the other
+  replicas' windows in place, ALLGATHER / TABLE emulate the collectives.
+  Checked against the oracle's G-rank emulation (oracle.train_step_dp), for
+  bit-identical replicas, and PEER == ALLGATHER bitwise.
+* a real one-rank NCCL communicator (pg_attach_nccl with world = 1): the
+  data-parallel code path, NCCL calls included, must equal the one-GPU step
+  bitwise (at G = 1 every rank-order sum is x + 0).
+"""
 import numpy as np
 import pytest
 
@@ -11,6 +19,7 @@ from tests._parity import assert_parity, oracle_from_gpu_params
 
 pytestmark = pytest.mark.gpu
 POLY = dict(V=100_000, d=64, n=5, h=32)
+MODES = {"peer": 1, "allgather": 2, "table": 3}
 
 
 @pytest.fixture(scope="module")
@@ -21,23 +30,100 @@ def pg():
     return pg
 
 
-@pytest.mark.parametrize("world,B_local", [(2, 512), (4, 256), (8, 1024)])
-def test_group_step_matches_oracle_dp(pg, world, B_local):
+def _saturated(V, d, n, h, seed=5):
+    return synth.random_params(V, d, n, h, seed=seed, w1_scale=200 * 0.5 / (n * d), w2_scale=200 * 0.5 / h)
+
+
+def _group(pg, world, mode, start=None, seed=42):
     V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
-    models = [pg.PolyglotModel(V, d, n, h, seed=42) for _ in range(world)]
-    p0 = models[0].get_params()
-    ref = oracle_from_gpu_params(p0, V, d, n, h)
+    ms = [pg.PolyglotModel(V, d, n, h, seed=seed, exchange=MODES[mode]) for _ in range(world)]
+    if start is not None:
+        for m in ms:
+            m.set_params(*start[:4], b2=start[4])
+    return ms
+
+
+def _run_group(pg, ms, world, B_local, steps, ref=None, seed=5, lr=0.1):
+    V, n = POLY["V"], POLY["n"]
     gl, rl = [], []
-    for t in range(4):
-        idx, corr = synth.batch(V, n, B_local * world, seed=5, step=t)
-        gl.append(pg.pg_train_step_group([m.handle for m in models], idx, corr, 0.1))
-        rl.append(oracle.train_step_dp(ref, idx, corr, 0.1, world))
-    outs = [m.get_params() for m in models]
-    for k in range(4):   # replicas bit-identical
-        for r in range(1, world):
+    for t in range(steps):
+        idx, corr = synth.batch(V, n, B_local * world, seed=seed, step=t)
+        gl.append(pg.pg_train_step_group([m.handle for m in ms], idx, corr, lr))
+        if ref is not None:
+            rl.append(oracle.train_step_dp(ref, idx, corr, lr, world))
+    return np.array(gl), np.array(rl)
+
+
+def _assert_replicas_equal(outs):
+    for k in range(4):
+        for r in range(1, len(outs)):
             assert np.array_equal(outs[0][k], outs[r][k]), (k, r)
-    assert_parity(np.array(gl), np.array(rl), p0, outs[0], ref, tau_delta=2e-3)
-    for m in models:
+
+
+@pytest.mark.parametrize("mode,world,B_local", [("peer", 2, 512), ("peer", 4, 256), ("peer", 8, 1024),
+                                                ("allgather", 4, 256), ("table", 4, 256)])
+def test_group_saturated_matches_oracle_dp(pg, mode, world, B_local):
+    # saturated regime (W1, w2 x200): updates far above the fp32 storage floor,
+    # so the embedding deltas are pinned at tau = 1e-4 (DESIGN.md §4 T3)
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    ms = _group(pg, world, mode, start=_saturated(V, d, n, h))
+    p0 = ms[0].get_params()
+    ref = oracle_from_gpu_params(p0, V, d, n, h)
+    gl, rl = _run_group(pg, ms, world, B_local, 6, ref)
+    outs = [m.get_params() for m in ms]
+    _assert_replicas_equal(outs)
+    rep = assert_parity(gl, rl, p0, outs[0], ref, tau_delta=1e-4)
+    print(mode, world, B_local, rep)
+    assert ms[0].exchange_info()[0] == mode
+    for m in ms:
+        m.close()
+
+
+@pytest.mark.parametrize("world,B_local", [(2, 512), (8, 1024)])
+def test_group_default_init_matches_oracle_dp(pg, world, B_local):
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    ms = _group(pg, world, "peer")
+    p0 = ms[0].get_params()
+    ref = oracle_from_gpu_params(p0, V, d, n, h)
+    gl, rl = _run_group(pg, ms, world, B_local, 4, ref)
+    outs = [m.get_params() for m in ms]
+    _assert_replicas_equal(outs)
+    assert_parity(gl, rl, p0, outs[0], ref, tau_delta=1e-3)
+    for m in ms:
+        m.close()
+
+
+def test_peer_equals_allgather_bitwise(pg):
+    # both sum each row's per-rank parts in rank order: the transport must not matter
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    res = {}
+    for mode in ("peer", "allgather"):
+        ms = _group(pg, 4, mode, start=_saturated(V, d, n, h, seed=8))
+        gl, _ = _run_group(pg, ms, 4, 512, 4)
+        res[mode] = (gl, ms[0].get_params())
+        for m in ms:
+            m.close()
+    assert np.array_equal(res["peer"][0], res["allgather"][0])
+    for k in range(4):
+        assert np.array_equal(res["peer"][1][k], res["allgather"][1][k]), k
+
+
+def test_group_g8_exchange_volume_and_owner_load(pg):
+    # merged per rank, G = 8 at 1024 examples per GPU moves
+    # ~3.0 MB of (row, gradient) entries into each rank per step (plus the
+    # 41 KB dense sums of 7 peers); no owner needs the sorted fallback (MCAP 512)
+    world, B_local, steps = 8, 1024, 3
+    ms = _group(pg, world, "peer")
+    for m in ms:
+        m.exchange_info(reset=True)
+    _run_group(pg, ms, world, B_local, steps)
+    stats = [m.exchange_info() for m in ms]
+    per_rank_step = [s[1] / steps for s in stats]
+    print("bytes/rank/step", per_rank_step, "max owner entries", [s[2] for s in stats])
+    for b in per_rank_step:
+        assert 2.0e6 < b < 3.6e6
+    assert max(s[2] for s in stats) <= 512
+    for m in ms:
         m.close()
 
 
@@ -45,31 +131,98 @@ def test_group_equals_single_step_semantics(pg):
     # G-rank DP on a batch == one step on the whole batch, up to fp32 reordering
     V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
     world, B_local = 4, 512
-    models = [pg.PolyglotModel(V, d, n, h, seed=3) for _ in range(world)]
+    ms = _group(pg, world, "peer", seed=3)
     single = pg.PolyglotModel(V, d, n, h, seed=3)
     idx, corr = synth.batch(V, n, B_local * world, seed=9)
-    lg = pg.pg_train_step_group([m.handle for m in models], idx, corr, 0.1)
+    lg = pg.pg_train_step_group([m.handle for m in ms], idx, corr, 0.1)
     ls = single.train_step(idx, corr, 0.1)
     assert abs(lg - ls) <= 1e-6 * abs(ls)
-    a, b = models[0].get_params(), single.get_params()
+    a, b = ms[0].get_params(), single.get_params()
     for k in range(4):
         assert np.abs(a[k] - b[k]).max() <= 1e-6 * max(1.0, np.abs(b[k]).max())
-    for m in models + [single]:
+    for m in ms + [single]:
         m.close()
 
 
-def test_group_bad_index_on_one_rank_skips_everyone(pg):
+def test_group_leaves_replica_settings(pg):
+    # a group step must not leave world / batch scaling / stream behind: a plain
+    # step afterwards equals the same step on a model that never joined a group
     V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    ms = _group(pg, 2, "peer", seed=4)
+    idx, corr = synth.batch(V, n, 512, seed=1)
+    pg.pg_train_step_group([m.handle for m in ms], idx, corr, 0.1)
+    fresh = pg.PolyglotModel(V, d, n, h, seed=4)
+    fresh.set_params(*ms[1].get_params()[:4], b2=ms[1].get_params()[4])
+    i2, c2 = synth.batch(V, n, 300, seed=2)
+    la, lb = ms[1].train_step(i2, c2, 0.1), fresh.train_step(i2, c2, 0.1)
+    assert la == lb
+    for k in range(4):
+        assert np.array_equal(ms[1].get_params()[k], fresh.get_params()[k])
+    for m in ms + [fresh]:
+        m.close()
+
+
+@pytest.mark.parametrize("mode", ["peer", "allgather", "table"])
+def test_group_bad_index_on_one_rank_skips_everyone(pg, mode):
+    V = POLY["V"]
     world, B_local = 2, 128
-    models = [pg.PolyglotModel(V, d, n, h, seed=1) for _ in range(world)]
-    p0 = [m.get_params() for m in models]
-    idx, corr = synth.batch(V, n, B_local * world, seed=2)
+    ms = _group(pg, world, mode, seed=1)
+    p0 = [m.get_params() for m in ms]
+    idx, corr = synth.batch(V, POLY["n"], B_local * world, seed=2)
     idx[B_local + 3, 2] = V + 7          # rank 1's shard
     with pytest.raises(pg.PGError) as e:
-        pg.pg_train_step_group([m.handle for m in models], idx, corr, 0.1)
+        pg.pg_train_step_group([m.handle for m in ms], idx, corr, 0.1)
     assert e.value.status == pg.PG_ERANGE
-    for r, m in enumerate(models):
+    for r, m in enumerate(ms):
         for a, b in zip(p0[r][:4], m.get_params()[:4]):
             assert np.array_equal(a, b)
-    for m in models:
+    # and the group keeps working
+    idx, corr = synth.batch(V, POLY["n"], B_local * world, seed=3)
+    pg.pg_train_step_group([m.handle for m in ms], idx, corr, 0.1)
+    for m in ms:
         m.close()
+
+
+@pytest.mark.parametrize("mode", ["peer", "allgather", "table"])
+def test_nccl_world1_equals_single_gpu_bitwise(pg, mode):
+    # a real one-rank NCCL communicator: dp_step with the NCCL calls (or the
+    # symmetric window) runs; every rank-order sum is x + 0, so the result is
+    # the one-GPU DET step bit for bit
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    dp = pg.PolyglotModel(V, d, n, h, seed=11, exchange=MODES[mode])
+    one = pg.PolyglotModel(V, d, n, h, seed=11)
+    start = _saturated(V, d, n, h, seed=6)
+    for m in (dp, one):
+        m.set_params(*start[:4], b2=start[4])
+    dp.attach_nccl(0, 1, pg.pg_nccl_unique_id())
+    for t in range(4):
+        idx, corr = synth.batch(V, n, 2048, seed=12, step=t)
+        a, b = dp.train_step(idx, corr, 0.1), one.train_step(idx, corr, 0.1)
+        assert a == b, (t, a, b)
+    for k in range(4):
+        assert np.array_equal(dp.get_params()[k], one.get_params()[k]), k
+    assert dp.exchange_info()[0] == mode
+    dp.close(); one.close()
+
+
+def test_nccl_world1_bad_index_and_divergence(pg):
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    m = pg.PolyglotModel(V, d, n, h, seed=2)
+    m.attach_nccl(0, 1, pg.pg_nccl_unique_id())
+    p0 = m.get_params()
+    idx, corr = synth.batch(V, n, 512, seed=1)
+    bad = idx.copy(); bad[9, 1] = -3
+    with pytest.raises(pg.PGError) as e:
+        m.train_step(bad, corr, 0.1)
+    assert e.value.status == pg.PG_ERANGE and "position 46 (value -3)" in str(e.value)
+    # saturated units and w2 = 1e37: every margin is ~1e38, the fp32 hinge sum
+    # overflows -> non-finite loss -> PG_EDIVERGED and nothing changes
+    C, W1, b1, w2, b2 = p0
+    big = (C, W1 * np.float32(1000), b1, np.full_like(w2, 1e37), b2)
+    m.set_params(*big[:4], b2=b2)
+    with pytest.raises(pg.PGError) as e:
+        m.train_step(idx, corr, 0.1)
+    assert e.value.status == pg.PG_EDIVERGED
+    for a, b in zip(big[:4], m.get_params()[:4]):
+        assert np.array_equal(a, b)
+    m.close()

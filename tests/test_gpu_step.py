@@ -287,3 +287,31 @@ def test_cuda_graph_capture_replay_equals_eager(pg):
     for a, b in zip(eager.get_params(), graphed.get_params()):
         assert np.array_equal(np.asarray(a), np.asarray(b))
     eager.close(); graphed.close()
+
+
+@pytest.mark.parametrize("scatter", [0, 1])
+@pytest.mark.parametrize("fused", [True, False])
+def test_nonfinite_loss_diverged_no_mutation(pg, scatter, fused):
+    # a non-finite loss -> PG_EDIVERGED and no parameter changes.
+    # Saturated units and w2 = 1e37: margins ~1e38, the fp32 hinge sum overflows.
+    m = make(pg, POLY, seed=2, scatter=scatter, fused=fused)
+    C, W1, b1, w2, b2 = m.get_params()
+    big = (C, W1 * np.float32(1000), b1, np.full_like(w2, 1e37))
+    m.set_params(*big, b2=b2)
+    idx, corr = synth.batch(POLY["V"], POLY["n"], 512, seed=1)
+    with pytest.raises(pg.PGError) as e:
+        m.train_step(idx, corr, 0.1)
+    assert e.value.status == pg.PG_EDIVERGED
+    for a, b in zip(big, m.get_params()[:4]):
+        assert np.array_equal(a, b)
+    # the literal north-star form returns NaN
+    assert np.isnan(pg.pg_train_step_loss(m.handle, idx, corr, 0.1))
+    # asynchronous steps make it sticky until pg_sync
+    m.train_step(idx, corr, 0.1, loss_out=None)
+    with pytest.raises(pg.PGError) as e:
+        m.sync()
+    assert e.value.status == pg.PG_EDIVERGED
+    m.sync()   # cleared
+    m.set_params(C, W1, b1, w2, b2)
+    m.train_step(idx, corr, 0.1)   # and the model keeps working
+    m.close()

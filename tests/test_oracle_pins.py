@@ -542,3 +542,23 @@ def test_train_step_is_theta_minus_lr_fd_gradient():
             assert (err <= tol).all(), f"{name}: max err {err.max():.3g} (seed {seed})"
         assert q.b2[0] == p.b2[0]
         good += 1
+
+
+def test_nonfinite_loss_is_diverged_and_changes_nothing():
+    # a non-finite loss is a divergence error and no parameter
+    # changes.  Saturated units and w2 = 3e307: margins reach ~1e308 and the
+    # hinge sum overflows float64.
+    V, d, n, h = 60, 4, 5, 8
+    p = oracle.Params.init(V, d, n, h, 4)
+    p.W1 *= 1000.0
+    p.w2[:] = 3e307
+    idx, corr = synth.batch(V, n, 64, seed=6)
+    q = p.copy()
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.train_step(q, idx, corr, 0.1)
+    assert e.value.status == 6
+    np.testing.assert_array_equal(q.flat(), p.flat())
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.train_step_dp(q, idx, corr, 0.1, world=2)
+    assert e.value.status == 6
+    np.testing.assert_array_equal(q.flat(), p.flat())
