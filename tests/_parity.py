@@ -24,25 +24,47 @@ def rel_inf(a, b):
     return 0.0 if den == 0.0 and num == 0.0 else num / max(den, 1e-300)
 
 
+def num_sms():
+    import torch
+    return torch.cuda.get_device_properties(0).multi_processor_count
+
+
+def chunk_row_counts(idx, corr, V, P, T):
+    """Per embedding row: the number of (CTA, chunk) lists of one step that
+    contain it -- exactly the number of red.global.add the ATOMIC step issues
+    for the row (each chunk pre-sums its duplicates; CTA p owns examples
+    [p*B/P, (p+1)*B/P) in chunks of T)."""
+    B = corr.shape[0]
+    cnt = np.zeros(V, np.int64)
+    for p in range(P):
+        lo, hi = p * B // P, (p + 1) * B // P
+        for e0 in range(lo, hi, T):
+            e1 = min(hi, e0 + T)
+            cnt[np.unique(np.concatenate([idx[e0:e1].ravel(), corr[e0:e1]]))] += 1
+    return cnt
+
+
 def run_both(model, V, d, n, h, B, steps, lr=0.1, seed=42, kind="sliding", start_params=None,
-             step0=0):
+             step0=0, chunk_T=32):
     """Drive the GPU model and the oracle through the same `steps` SGD steps.
 
-    Returns (gpu_losses, ref_losses, p0 (float32 tuple), gpu_params_end, oracle Params)."""
+    Returns (gpu_losses, ref_losses, p0 (float32 tuple), gpu_params_end, oracle Params).
+    run_both.roundings: per embedding row, the red.adds an ATOMIC step issues
+    (chunk_row_counts summed over the steps; chunk_T = the path's chunk size)."""
     import paper_1404_1521_b200 as pg
     if start_params is not None:
         pg.pg_set_params(model.handle, *start_params[:4], b2=start_params[4])
     p0 = pg.pg_get_params(model.handle)
     ref = oracle_from_gpu_params(p0, V, d, n, h)
     gl, rl = [], []
-    occ = np.zeros(V, np.int64)     # embedding-row occurrences (bounds atomic roundings)
+    rnd = np.zeros(V, np.int64)     # red.adds per embedding row (ATOMIC roundings)
+    P = min(num_sms(), B)
     for t in range(steps):
         idx, corr = synth.batch(V, n, B, seed=seed, step=step0 + t, kind=kind)
         gl.append(model.train_step(idx, corr, lr))
         rl.append(oracle.train_step(ref, idx, corr, lr))
-        np.add.at(occ, idx.ravel(), 1)
-        np.add.at(occ, corr, 1)
-    run_both.occurrences = occ
+        rnd += chunk_row_counts(idx, corr, V, P, chunk_T)
+    run_both.roundings = rnd
     return np.array(gl), np.array(rl), p0, pg.pg_get_params(model.handle), ref
 
 
@@ -56,8 +78,8 @@ def assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3, tol=1e-4, c_roundings=N
     allowance the delta check measures storage rounding, not the kernel
     (DESIGN.md "Parity tolerances").  The saturated-regime test keeps updates
     far above the storage floor and runs with tau = 1e-4.  In atomic mode every
-    red.add rounds the stored row, so c_roundings (per embedding row: an upper
-    bound on the number of red.adds, its occurrence count) replaces `steps`."""
+    red.add rounds the stored row, so c_roundings (per embedding row: the
+    number of red.adds issued, run_both.roundings) replaces `steps`."""
     rel_loss = np.abs(gl - rl) / np.maximum(np.abs(rl), 1e-30)
     assert rel_loss.max() <= tol, f"T1 loss rel err {rel_loss.max():.3g}"
     C, W1, b1, w2, b2 = pend
@@ -82,3 +104,18 @@ def assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3, tol=1e-4, c_roundings=N
             assert e_delta <= tau_delta, f"T3 {k} delta: {e_delta:.3g}"
     assert b2 == p0[4], "T4: b2 must never change"
     return report
+
+
+def higham_bound(W0, Y, I):
+    """Rigorous bound on |fp32 W[I] += Y - exact| per element, for ANY
+    summation order of a row's m contributions (W0 included): gamma_m *
+    (|W0| + sum |Y|) with gamma_m = m u / (1 - m u), u = 2^-24 (Higham,
+    recursive summation), plus the fp32 rounding of the stored result."""
+    u = 2.0 ** -24
+    I = np.asarray(I, np.int64)
+    absum = np.abs(W0).astype(np.float64)
+    np.add.at(absum, I, np.abs(Y).astype(np.float64))
+    m = np.ones(W0.shape[0], np.float64)
+    np.add.at(m, I, 1.0)
+    gam = (m * u / (1 - m * u))[:, None]
+    return gam * absum + u * absum

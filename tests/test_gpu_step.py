@@ -48,7 +48,7 @@ def test_tiny_100_steps(pg, scatter):
     m = make(pg, TINY, scatter=scatter)
     gl, rl, p0, pend, ref = run_both(m, **TINY, B=16, steps=100)
     rep = assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3,
-                        c_roundings=run_both.occurrences if scatter else None)
+                        c_roundings=run_both.roundings if scatter else None)
     print("tiny", scatter, rep)
     m.close()
 
@@ -56,9 +56,9 @@ def test_tiny_100_steps(pg, scatter):
 @pytest.mark.parametrize("scatter", [0, 1])
 def test_polyglot_b1024_default_init(pg, scatter):
     m = make(pg, POLY, scatter=scatter)
-    gl, rl, p0, pend, ref = run_both(m, **POLY, B=1024, steps=10)
+    gl, rl, p0, pend, ref = run_both(m, **POLY, B=1024, steps=20)
     rep = assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3,
-                        c_roundings=run_both.occurrences if scatter else None)
+                        c_roundings=run_both.roundings if scatter else None)
     print("poly", scatter, rep)
     m.close()
 
@@ -69,11 +69,11 @@ def test_polyglot_saturated_regime(pg, scatter):
     V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
     start = synth.random_params(V, d, n, h, seed=5, w1_scale=200 * 0.5 / (n * d), w2_scale=200 * 0.5 / h)
     m = make(pg, POLY, scatter=scatter)
-    gl, rl, p0, pend, ref = run_both(m, V, d, n, h, B=1024, steps=10, start_params=start)
+    gl, rl, p0, pend, ref = run_both(m, V, d, n, h, B=1024, steps=20, start_params=start)
     f = oracle.forward(oracle_from_gpu_params(p0, V, d, n, h), *synth.batch(V, n, 1024, seed=42, step=0))
     assert (np.abs(f["a"]) > 1).mean() > 0.2          # really saturated
     rep = assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-4,
-                        c_roundings=run_both.occurrences if scatter else None)
+                        c_roundings=run_both.roundings if scatter else None)
     print("sat", scatter, rep)
     m.close()
 
@@ -83,7 +83,23 @@ def test_ragged_batches(pg, B):
     # ragged tails, fewer examples than SMs, and several chunks per CTA (B > 148*32)
     m = make(pg, POLY)
     gl, rl, p0, pend, ref = run_both(m, **POLY, B=B, steps=3, kind="iid")
-    assert_parity(gl, rl, p0, pend, ref, tau_delta=2e-3)
+    assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3)
+    m.close()
+
+
+SAT = lambda V, d, n, h, seed=5: synth.random_params(V, d, n, h, seed=seed, w1_scale=200 * 0.5 / (n * d),
+                                                      w2_scale=200 * 0.5 / h)
+
+
+@pytest.mark.parametrize("scatter", [0, 1])
+@pytest.mark.parametrize("B", [1, 7, 149, 1000, 4096 + 37, 9000])
+def test_ragged_batches_saturated(pg, B, scatter):
+    # the ragged shapes in the saturated regime: embedding updates far above the
+    # fp32 storage floor, so T3 pins every tensor's delta at tau = 1e-4
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    m = make(pg, POLY, scatter=scatter)
+    gl, rl, p0, pend, ref = run_both(m, V, d, n, h, B=B, steps=3, kind="iid", start_params=SAT(V, d, n, h))
+    assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-4, c_roundings=run_both.roundings if scatter else None)
     m.close()
 
 
@@ -197,9 +213,21 @@ def test_large_shape_generic_path(pg):
     # BASELINE.json configs[4] shape (V 1M, d 128, h 128) on one GPU, small batch
     V, d, n, h = 1_000_000, 128, 5, 128
     m = pg.PolyglotModel(V, d, n, h, seed=3)
-    gl, rl, p0, pend, ref = run_both(m, V, d, n, h, B=512, steps=2)
+    gl, rl, p0, pend, ref = run_both(m, V, d, n, h, B=512, steps=3)
     assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3)
     m.close()
+
+
+def test_large_shape_saturated(pg):
+    # the large config's shape at its per-GPU batch (4096 / 8 = 512) and at 4096,
+    # saturated regime: T3 at tau = 1e-4 pins the embedding update
+    V, d, n, h = 1_000_000, 128, 5, 128
+    start = SAT(V, d, n, h, seed=7)
+    for B, steps in ((512, 3), (4096, 2)):
+        m = pg.PolyglotModel(V, d, n, h, seed=3)
+        gl, rl, p0, pend, ref = run_both(m, V, d, n, h, B=B, steps=steps, start_params=start)
+        assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-4)
+        m.close()
 
 
 def test_owner_overflow_sorted_fallback(pg):

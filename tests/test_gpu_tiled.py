@@ -31,7 +31,7 @@ def test_tiled_parity(pg, cfg, B):
     # B = 2413 > 148 * 16: several 16-example chunks per CTA (record RMW path)
     m = pg.PolyglotModel(cfg["V"], cfg["d"], cfg["n"], cfg["h"], seed=11)
     gl, rl, p0, pend, ref = run_both(m, **cfg, B=B, steps=3, kind="iid" if B < 100 else "sliding")
-    assert_parity(gl, rl, p0, pend, ref, tau_delta=2e-3)
+    assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3)
     m.close()
 
 
@@ -78,14 +78,18 @@ def test_tiled_bad_index_and_set_params(pg):
     m.set_params(*start)
     gl, rl, q0, qend, ref = run_both(m, V, d, n, h, B=500, steps=2)
     assert np.array_equal(q0[1], start[1].astype(np.float32))
-    assert_parity(gl, rl, q0, qend, ref, tau_delta=2e-3)
+    assert_parity(gl, rl, q0, qend, ref, tau_delta=1e-3)
     m.close()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_tiled_group_step_matches_oracle_dp(pg, world):
+@pytest.mark.parametrize("world,sat", [(2, False), (4, False), (4, True)])
+def test_tiled_group_step_matches_oracle_dp(pg, world, sat):
     V, d, n, h = 20_000, 64, 5, 128
     models = [pg.PolyglotModel(V, d, n, h, seed=42) for _ in range(world)]
+    if sat:
+        start = synth.random_params(V, d, n, h, seed=5, w1_scale=200 * 0.5 / (n * d), w2_scale=200 * 0.5 / h)
+        for mm in models:
+            mm.set_params(*start[:4], b2=start[4])
     p0 = models[0].get_params()
     ref = oracle_from_gpu_params(p0, V, d, n, h)
     gl, rl = [], []
@@ -97,6 +101,6 @@ def test_tiled_group_step_matches_oracle_dp(pg, world):
     for k in range(4):
         for r in range(1, world):
             assert np.array_equal(outs[0][k], outs[r][k]), (k, r)
-    assert_parity(np.array(gl), np.array(rl), p0, outs[0], ref, tau_delta=2e-3)
+    assert_parity(np.array(gl), np.array(rl), p0, outs[0], ref, tau_delta=1e-4 if sat else 1e-3)
     for mm in models:
         mm.close()
