@@ -154,14 +154,29 @@ def oracle_rate(B, steps, seed=42, warmup=0):
     return B * steps / dt, dt
 
 
+def host_info():
+    """Host CPU of this box (the oracle baselines' context)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"host_nproc": os.cpu_count(), "host_cpu_model": model}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    # each step: one oracle SGD step on a bounded sample (batch <= 1024, ~50 ms)
-    steps = max(1, min(args.steps, 200))
-    warm = max(0, min(args.warmup, 5))
-    B = min(args.batch, 1024)
+    # each step: one oracle SGD step of the bench's own workload (batch 4096 per
+    # GPU, ~0.2 s of float64 on one host thread), at most 40 timed steps
+    steps = max(1, min(args.steps, 40))
+    warm = max(0, min(args.warmup, 3))
+    B = args.batch
     rate, dt = oracle_rate(B, steps, warmup=warm)
     cfg = {"workload": f"polyglot_v100k_d64_n5_h32_b{args.batch}", "vocab": POLY["V"], "dim": POLY["d"],
            "window": POLY["n"], "hidden": POLY["h"], "batch_per_gpu": args.batch,
@@ -172,7 +187,8 @@ def run_reference(args):
         "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": rate, "unit": "examples/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{steps} SGD steps of batch {B} (Polyglot shape), float64, 1 thread"},
+                         "sample": f"{steps} SGD steps of batch {B} (Polyglot shape), float64, 1 thread",
+                         **host_info()},
         "e2e": {"value": rate, "unit": "examples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -235,6 +251,11 @@ def main():
         barrier()
     launches = model.kernel_launches() - l0
     model.sync()
+    xinfo = None
+    if world > 1:   # the data-parallel exchange the library chose, and its volume
+        mode_name, xbytes, xmax = model.exchange_info()
+        xinfo = {"mode": mode_name, "bytes_read_per_rank_per_step": xbytes / max(1, args.warmup + args.steps),
+                 "max_owner_entries": xmax}
     times = [a.elapsed_time(b) for a, b in ev]          # ms
     tot_ms = sum(times)
     if world > 1:
@@ -340,10 +361,13 @@ def main():
             "peaks": {"source": peak_kind, "hbm_gbs": peaks.get("hbm_gbs")},
         }
         out.update(extras)
+        if world > 1:
+            out["exchange"] = xinfo
         if not args.no_cpu_baseline and world == 1:   # the oracle's host baseline: N = 1 only
-            rate, dt = oracle_rate(1024, 25)
+            rate, dt = oracle_rate(B, 12)
             out["cpu_baseline"] = {"value": rate, "unit": "examples/s", "cores": 1, "kind": "oracle",
-                                   "sample": "25 SGD steps x batch 1024 (Polyglot shape), float64, 1 host thread"}
+                                   "sample": f"12 SGD steps x batch {B} (the bench workload), float64, "
+                                             "1 host thread", **host_info()}
         print(json.dumps(out), flush=True)
     model.close()
     if world > 1:
@@ -487,8 +511,48 @@ def run_extras(pg, torch, synth, np, dev, stream, flush, model):
     big.close()
     res["large_config"] = {"config": "V 1M, d 128, n 5, h 128 (BASELINE.json configs[3] shape), L2 flushed, 1 GPU",
                            "path": "tiled phase 1 (FFMA2)", "results": lg}
+    res["dp_exchange_emulated"] = dp_emulation(pg, torch, synth, dev, stream)
     res["oracle_timings"] = oracle_timings(np, synth)
     return res
+
+
+def dp_emulation(pg, torch, synth, dev, stream):
+    """BASELINE.json configs[3] (global batch 8192 over G GPUs) emulated on this
+    one GPU: G replicas run the data-parallel kernels (PEER exchange: the
+    replicas' windows read in place), so the per-rank exchange volume and owner
+    load are the real ones.  The G replicas run one after another here: the time
+    is NOT a multi-GPU number (the driver's scaling run measures that)."""
+    V, d, n, h = POLY["V"], POLY["d"], POLY["n"], POLY["h"]
+    out = {}
+    for G in (2, 4, 8):
+        Bl = 8192 // G
+        ms = [pg.PolyglotModel(V, d, n, h, seed=42, stream=stream, exchange=pg.PG_EXCHANGE_PEER) for _ in range(G)]
+        bs = [synth.batch(V, n, 8192, seed=9, step=t) for t in range(6)]
+        di = [torch.from_numpy(i).to(dev) for i, _ in bs]
+        dc = [torch.from_numpy(c).to(dev) for _, c in bs]
+        handles = [m.handle for m in ms]
+        for t in range(2):
+            pg.pg_train_step_group(handles, di[t], dc[t], 0.1)
+        for m in ms:
+            m.exchange_info(reset=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for t in range(2, 6):
+            pg.pg_train_step_group(handles, di[t], dc[t], 0.1)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / 4
+        st = [m.exchange_info() for m in ms]
+        # what one rank would move with the NCCL exchanges at this shape (bytes received)
+        rec = (n + 1) * Bl * (4 + 4 * d) + 148 * 16
+        out[f"G{G}_Blocal{Bl}"] = {
+            "exchange": st[0][0], "bytes_read_per_rank_per_step": sum(s[1] for s in st) / len(st) / 4,
+            "max_owner_entries": max(s[2] for s in st),
+            "nccl_allgather_bytes_per_rank_per_step": (G - 1) * rec,
+            "nccl_table_allreduce_bytes_per_rank_per_step": 2 * (G - 1) / G * V * d * 4,
+            "group_step_ms_one_gpu_sequential": dt * 1e3}
+        for m in ms:
+            m.close()
+    return out
 
 
 if __name__ == "__main__":

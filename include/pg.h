@@ -80,7 +80,10 @@ enum {
                          0: two ordinary kernels (phase 1 | phase 2), same results */
   PG_OPT_RESERVE = 4, /* value: batch size; allocates the step workspace for it now
                          (so later steps at <= that batch never allocate -- e.g.
-                         before CUDA-graph capture).  PG_EINVAL unless 1..2^30. */
+                         before CUDA-graph capture).  After pg_attach_nccl it also
+                         sets up the data-parallel exchange for exactly that batch
+                         and is then collective (every rank, same value).
+                         PG_EINVAL unless 1..2^30. */
   PG_OPT_TRACE = 5,   /* value: (int64_t) device pointer to >= 64*P uint64 slots, 0 = off.
                          Per-CTA %globaltimer stamps of the step's stages; honoured
                          only by the instrumented build libpg_trace.so (-DPG_TRACE),

@@ -394,6 +394,8 @@ extern "C" pg_status pg_get_shape(const pg_model* m, int64_t* vocab, int32_t* di
   return PG_OK;
 }
 
+static pg_status ensure_dp(pg_model* m, int B);
+
 extern "C" pg_status pg_set_option(pg_model* m, int key, int64_t value) {
   if (pg_status s = check_model(m)) return s;
   switch (key) {
@@ -436,7 +438,8 @@ extern "C" pg_status pg_set_option(pg_model* m, int key, int64_t value) {
     case PG_OPT_RESERVE: {   // pre-size the workspace for a batch
       if (value < 1 || value > (1 << 30)) return fail(PG_EINVAL, "reserve: bad batch");
       if (pg_status s = set_device(m)) return s;
-      return ensure_ws(m, (int)value);
+      if (pg_status s = ensure_ws(m, (int)value, m->world)) return s;
+      return m->comm ? ensure_dp(m, (int)value) : PG_OK;   // collective after pg_attach_nccl
     }
     default:
       return fail(PG_EINVAL, "pg_set_option: unknown key %d", key);
@@ -545,7 +548,7 @@ extern "C" pg_status pg_train_step(pg_model* m, const int32_t* idx_batch, const 
   if (batch < 1) return fail(PG_EINVAL, "pg_train_step: empty batch (batch=%d); the loss is undefined", batch);
   if (!std::isfinite(lr) || !(lr > 0.f)) return fail(PG_EINVAL, "pg_train_step: lr must be finite and > 0 (got %g)", lr);
   if (pg_status s = set_device(m)) return s;
-  if (pg_status s = ensure_ws(m, batch)) return s;
+  if (pg_status s = ensure_ws(m, batch, m->world)) return s;
   const PtrKind kl = ptr_kind(loss_out);
   const int32_t *di = nullptr, *dc = nullptr;
   if (pg_status s = stage_inputs(m, idx_batch, corrupt_idx, batch, &di, &dc)) return s;
