@@ -2139,13 +2139,29 @@ __global__ void dp_table_apply_kernel(StepParams p, float* table, int zero) {
 }
 
 // ------------------------------------------------------------------ kernels
-template <int PATH, int DP>   // PATH: 0 generic, 1 fast (h == 32), 2/3/4 tiled with 16/4/8-example chunks
-__global__ void __launch_bounds__(384, 1) step_kernel(StepParams p, int phases) {
+// PATH: 0 generic, 1 fast (h == 32), 2/3/4 tiled with 16/4/8-example chunks,
+// 5 the fast path specialised to the Polyglot shape (d 64, n 5, h 32: the
+// shape and the shape-only shared-memory offsets become compile-time
+// constants, which removes most index arithmetic and shrinks the executed
+// code -- the step is latency-bound and its code is fetched once per launch).
+// ACT: the nonlinearity (PG_OPT_ACTIVATION), so a kernel carries one.
+template <int PATH, int DP, int ACT>
+__global__ void __launch_bounds__(384, 1) step_kernel(StepParams p_in, int phases) {
   extern __shared__ __align__(16) unsigned char smem[];
+  StepParams p = p_in;
+  p.act = ACT;
+  if (PATH == 5) {
+    p.d = 64; p.n = 5; p.h = 32; p.T = kTMax;
+    const Layout L = make_layout(64, 5, 32, kTMax, 384, 0, 1);
+    const int lbase = p.lay.lbase, loff = p.lay.loff;
+    p.lay = L;
+    p.lay.lbase = lbase;
+    p.lay.loff = loff;
+  }
   trace_mark(p, 0);
   trace_clock(p, 12);
   if (phases & 1) {
-    if (PATH == 1) phase1_fast(p, smem);
+    if (PATH == 1 || PATH == 5) phase1_fast(p, smem);
     else if (PATH == 2) phase1_tiled_t<kTT>(p, smem);
     else if (PATH == 3) phase1_tiled_t<kTTSmall>(p, smem);
     else if (PATH == 4) phase1_tiled_t<kTTMid>(p, smem);
@@ -2203,42 +2219,52 @@ int step_chunk_T(int d, int n, int h, int fast, int per_cta) {
   return T;
 }
 
+static bool poly_shape(int d, int n, int h) { return d == 64 && n == 5 && h == 32; }
+
 // The tiled path has one kernel per chunk size, so neither carries the other's
 // code (a combined kernel ran the 16-example case 12 % slower); the data-
 // parallel phases live in their own instantiations (DP = 1), so the one-GPU
-// kernel carries none of their code either.
-template <int DP>
-static const void* step_fn_t(int fast, int T) {
+// kernel carries none of their code either; likewise one kernel per
+// nonlinearity, and the Polyglot shape has its own (PATH 5).
+template <int DP, int ACT>
+static const void* step_fn_t(int fast, int T, bool poly) {
   if (fast == 2)
-    return T == kTTSmall ? (const void*)step_kernel<3, DP>
-           : T == kTTMid ? (const void*)step_kernel<4, DP>
-                         : (const void*)step_kernel<2, DP>;
-  return fast == 1 ? (const void*)step_kernel<1, DP> : (const void*)step_kernel<0, DP>;
+    return T == kTTSmall ? (const void*)step_kernel<3, DP, ACT>
+           : T == kTTMid ? (const void*)step_kernel<4, DP, ACT>
+                         : (const void*)step_kernel<2, DP, ACT>;
+  if (fast == 1) return poly ? (const void*)step_kernel<5, DP, ACT> : (const void*)step_kernel<1, DP, ACT>;
+  return (const void*)step_kernel<0, DP, ACT>;
 }
-static const void* step_fn(int fast, int T, int dp) { return dp ? step_fn_t<1>(fast, T) : step_fn_t<0>(fast, T); }
+static const void* step_fn(int fast, int T, int dp, int act, bool poly) {
+  if (dp) return act ? step_fn_t<1, 1>(fast, T, poly) : step_fn_t<1, 0>(fast, T, poly);
+  return act ? step_fn_t<0, 1>(fast, T, poly) : step_fn_t<0, 0>(fast, T, poly);
+}
 
 // Allow up to the opt-in maximum minus the kernel's static shared memory.
 cudaError_t step_prepare(int fast, size_t optin, size_t* usable) {
   size_t best = optin;
   for (int dp = 0; dp < 2; ++dp)
-    for (int T : {kTT, kTTSmall, kTTMid}) {
-      const void* fn = step_fn(fast, T, dp);
-      cudaFuncAttributes fa;
-      cudaError_t e = cudaFuncGetAttributes(&fa, fn);
-      if (e != cudaSuccess) return e;
-      const size_t smem = optin - fa.sharedSizeBytes;
-      if (smem < best) best = smem;
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      if (fast != 2) break;
-    }
+    for (int act = 0; act < 2; ++act)
+      for (int poly = 0; poly < (fast == 1 ? 2 : 1); ++poly)
+        for (int T : {kTT, kTTSmall, kTTMid}) {
+          const void* fn = step_fn(fast, T, dp, act, poly != 0);
+          cudaFuncAttributes fa;
+          cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+          if (e != cudaSuccess) return e;
+          const size_t smem = optin - fa.sharedSizeBytes;
+          if (smem < best) best = smem;
+          e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          if (e != cudaSuccess) return e;
+          if (fast != 2) break;
+        }
   if (usable) *usable = best;
   return cudaSuccess;
 }
 
 void launch_step_phases(const StepParams& p, int phases, int fast, cudaStream_t s, int* launches) {
   const int NT = step_block_threads(p.d, p.n, p.h, fast);
-  const void* fn = step_fn(fast, p.T, (phases & 24) != 0);
+  const bool poly = fast == 1 && poly_shape(p.d, p.n, p.h) && p.T == kTMax && NT == 384;
+  const void* fn = step_fn(fast, p.T, (phases & 24) != 0, p.act, poly);
   void* args[] = {(void*)&p, (void*)&phases};
   if ((phases & 1) && (phases & 10)) cudaLaunchCooperativeKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
   else cudaLaunchKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);

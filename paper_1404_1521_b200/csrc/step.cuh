@@ -111,10 +111,10 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.ws = o;    o = align16(o + 64 * 4);
   L.red = o;   o = align16(o + 2 * 32 * 32 * 4);
   L.total1 = o;
-  // phase 2 (aliases phase 1 storage)
+  // phase 2 (aliases phase 1 storage); the per-list tables (sized by the
+  // list count) go last, so every other offset depends on the shape only
+  // and a shape-specialised kernel can fold them (step_kernel PATH 5)
   o = 32;
-  L.lbase = o; o = align16(o + (NLtot + 1) * 4);
-  L.loff = o;  o = align16(o + (NLtot + 1) * 4);
   L.ws2 = o;   o = align16(o + 64 * 4);
   L.dred = o;  o = align16(o + NT * 16);
   const int p2fixed = o;
@@ -153,7 +153,10 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.SB = SB;
   L.stagefb = o; o = align16(o + SB * d * 4);
   L.carry = o; o = align16(o + 2 * 4 * d * 4);   // [2][4 chains][d]
-  L.total2 = o > fast_end ? o : fast_end;
+  o = o > fast_end ? o : fast_end;
+  L.lbase = o; o = align16(o + (NLtot + 1) * 4);
+  L.loff = o;  o = align16(o + (NLtot + 1) * 4);
+  L.total2 = o;
   return L;
 }
 
