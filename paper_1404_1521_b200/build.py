@@ -24,7 +24,7 @@ def paths(variant: str = ""):
     if variant == "trace":
         return os.path.join(HERE, "_build_trace"), os.path.join(HERE, "libpg_trace.so"), ["-DPG_TRACE"]
     return BUILD, LIB, []
-SOURCES = ["api.cu", "step.cu", "scatter.cu", "nccl_shim.cpp", "nccl_lsa.cu"]
+SOURCES = ["api.cu", "step.cu", "scatter.cu", "scatter_det.cu", "nccl_shim.cpp", "nccl_lsa.cu"]
 HEADERS = ["common.cuh", "step.cuh", "scatter.cuh", "nccl_shim.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -3,7 +3,10 @@
 // and for each row, each cell in the row is added in parallel")
 // as two sm_100a pipelines behind pg_scatter_add:
 //
-// DET (bit-reproducible): stable LSD radix sort of (I[k], k) in passes of
+// DET (bit-reproducible), n <= P * 8192 (P = SM count): one cooperative launch
+//   (sc_det_owner, scatter_det.cu): bucket sort by owner CTA, per-owner stable
+//   sort by row, segmented reduction; Zipf head rows split by position.
+// DET, larger n (or PG_SC_DET_SORT set): stable LSD radix sort of (I[k], k) in passes of
 //   <= 10-bit digits -- per pass an upsweep (per-tile digit counts), a
 //   two-launch scan of the digit-major count matrix and a downsweep (stable
 //   in-tile ranks by warp ballots, staged in smem, coalesced write-out) --
@@ -19,6 +22,7 @@
 //   guarantee.
 #include "common.cuh"
 #include "scatter.cuh"
+#include <cstdlib>
 
 namespace pg {
 
@@ -976,6 +980,13 @@ ScatterPlan scatter_plan(int64_t rows, int cols, int64_t n, int num_sms) {
   pl.off_carry = take(sizeof(float) * 2 * pl.nchunks * cols);
   pl.off_cfk = take(sizeof(int) * pl.nchunks);
   pl.off_clk = take(sizeof(int) * pl.nchunks);
+  pl.det_owner = det_owner_ok(rows, cols, n, num_sms) && !getenv("PG_SC_DET_SORT");
+  if (pl.det_owner) {
+    pl.off_bucket = take(sizeof(int2) * n);
+    pl.off_hcnt = take(sizeof(unsigned) * num_sms * num_sms);
+    pl.off_hpart = take(sizeof(float) * det_owner_hpart_floats(num_sms, cols));
+    pl.off_hmask = take(sizeof(int) * det_owner_hmask_ints(num_sms));
+  }
   pl.total_bytes = o;
   return pl;
 }
@@ -1016,6 +1027,17 @@ cudaError_t scatter_launch(const ScatterPlan& pl, void* ws, float* W, int64_t ro
     *launches += 1;
     *slot = par;
     return cudaLaunchCooperativeKernel(kHotFn, pl.num_sms, kHotThreads, args, smem, s);
+  }
+  if (mode == 0 && pl.det_owner) {
+    const int par = (int)(epoch & 1);
+    *launches += 1;
+    *slot = par;
+    static const long long ypf_mb = getenv("PG_SC_YPF_MB") ? atoll(getenv("PG_SC_YPF_MB")) : 0;
+    int64_t ypf = (int64_t)(ypf_mb << 20) >> 7;
+    if (ypf > (n * cols * (int64_t)sizeof(float)) >> 7) ypf = (n * cols * (int64_t)sizeof(float)) >> 7;
+    return det_owner_launch(I, Y, W, rows, cols, n, st, par, reinterpret_cast<int2*>(b + pl.off_bucket),
+                            reinterpret_cast<unsigned*>(b + pl.off_hcnt), reinterpret_cast<float*>(b + pl.off_hpart),
+                            reinterpret_cast<int*>(b + pl.off_hmask), pl.num_sms, ypf, s);
   }
   e = cudaMemsetAsync(b, 0, pl.zero_bytes, s);
   if (e != cudaSuccess) return e;
@@ -1101,6 +1123,7 @@ cudaError_t scatter_prepare(int bins) {
                              (int)(sizeof(int) * (kSortThreads / 32) * bins));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(kHotFn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHotSmemMax);
+  if (e == cudaSuccess) e = det_owner_prepare();
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sc_reduce<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reduce_smem(4));
   if (e == cudaSuccess)

@@ -24,7 +24,19 @@ struct ScatterPlan {
   int64_t ntiles, nchunks;
   size_t off_status, off_hist, off_ctr, off_lookback, zero_bytes;
   size_t off_ka, off_va, off_kb, off_vb, off_carry, off_cfk, off_clk, off_rep, total_bytes;
+  // DET owner-bucket kernel (scatter_det.cu): used when det_owner is set
+  int det_owner;
+  size_t off_bucket, off_hcnt, off_hpart, off_hmask;
 };
+
+// scatter_det.cu
+bool det_owner_ok(int64_t rows, int cols, int64_t n, int P);
+size_t det_owner_hpart_floats(int P, int cols);
+size_t det_owner_hmask_ints(int P);
+cudaError_t det_owner_prepare();
+cudaError_t det_owner_launch(const int32_t* I, const float* Y, float* W, int64_t rows, int cols, int64_t n,
+                             ScatterStatus* st, int par, int2* bucket, unsigned* Hcnt, float* hpart, int* hmask,
+                             int P, int64_t ypf_lines, cudaStream_t s);
 
 ScatterPlan scatter_plan(int64_t rows, int cols, int64_t n, int num_sms);
 int scatter_supported(int cols, int mode);
