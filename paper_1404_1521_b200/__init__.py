@@ -22,6 +22,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # PG_LIB_VARIANT=trace selects the instrumented build (libpg_trace.so, see build.py)
 LIB_PATH = os.path.join(_HERE, "libpg_trace.so" if os.environ.get("PG_LIB_VARIANT") == "trace" else "libpg.so")
+# PG_LIB_PATH overrides it (A/B experiments: scripts/ab_variant.py builds variant libraries)
+LIB_PATH = os.environ.get("PG_LIB_PATH", LIB_PATH)
 
 PG_OK, PG_EINVAL, PG_ERANGE, PG_ENOMEM, PG_ECUDA, PG_ENCCL, PG_EDIVERGED = range(7)
 PG_SCATTER_DET, PG_SCATTER_ATOMIC = 0, 1

@@ -40,6 +40,10 @@
 #include "common.cuh"
 #include "scatter.cuh"
 
+#ifndef PG_OPF
+#define PG_OPF 2
+#endif
+
 namespace pg {
 
 #ifdef PG_TRACE
@@ -208,6 +212,18 @@ __device__ void o_segreduce(int cnt, Ent&& ent, const float4* __restrict__ Y, in
       uint2 mn[kOU];
 #pragma unroll
       for (int u = 0; u < kOU; ++u) mn[u] = i0 + kOU + u < e ? ent(i0 + kOU + u) : make_uint2(0u, kEnd);
+#if PG_OPF > 0
+      if (gl == 0) {   // rows PG_OPF batches ahead start moving into L2 (no registers held)
+#pragma unroll
+        for (int u = 0; u < kOU; ++u) {
+          const int ip = i0 + (1 + PG_OPF) * kOU + u;
+          if (ip < e) {
+            const char* yr = reinterpret_cast<const char*>(Y + (size_t)ent(ip).x * q);
+            for (int off = 0; off < 16 * q; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(yr + off));
+          }
+        }
+      }
+#endif
 #pragma unroll
       for (int u = 0; u < kOU; ++u) {
         if (m[u].y == kEnd) break;
