@@ -53,6 +53,9 @@ struct pg_model {
   int d = 0, n = 0, h = 0;
   float *C = nullptr, *W1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;
   float* W1T = nullptr;   // tiled path: W1 transposed [h][n*d]
+  float* xg = nullptr;    // tiled path, small chunks: [B][n+1][d] inputs for the phase-2 dW1 GEMM
+  float* sg = nullptr;    //   and [B][3][h] deltas
+  int64_t cap_xg = 0;     //   examples they hold
   DevStatus* st = nullptr;
   DevStatus* st_host = nullptr;  // pinned mirror for blocking reads
   cudaStream_t stream = nullptr;
@@ -216,6 +219,7 @@ static void free_ws(pg_model* m) {
 
 struct Geometry {
   int P, R, T, cap, NL, dense_len, dense_stride;
+  int dw1_gemm;   // tiled path with small chunks (one GPU): dW1 as a phase-2 GEMM
   size_t smem;
   Layout lay;
 };
@@ -229,6 +233,7 @@ static Geometry geometry(const pg_model* m, int B, int world = 1) {
   g.cap = (m->n + 1) * g.T;
   g.NL = g.P * g.R;
   g.dense_len = m->n * m->d * m->h + 2 * m->h;
+  g.dw1_gemm = world == 1 && step_dw1_gemm(m->fast, g.T);
   g.dense_stride = ((g.dense_len + 2) + 3) & ~3;   // dense | hinge | flags
   g.lay = make_layout(m->d, m->n, m->h, g.T, step_block_threads(m->d, m->n, m->h, m->fast),
                       g.NL > world ? g.NL : world, m->fast);
@@ -252,6 +257,14 @@ static pg_status ensure_ws(pg_model* m, int B, int world = 1) {
     CU(cudaMalloc(&m->list_vals, sizeof(float) * L * m->d));
     CU(cudaMalloc(&m->list_off, sizeof(int32_t) * off));
     m->cap_lists = L; m->cap_dense = dense; m->cap_off = off;
+  }
+  if (g.dw1_gemm && B > m->cap_xg) {
+    CU(cudaStreamSynchronize(m->stream));
+    cudaFree(m->xg); cudaFree(m->sg);
+    m->xg = m->sg = nullptr;
+    CU(cudaMalloc(&m->xg, sizeof(float) * (size_t)(m->n + 1) * m->d * B));
+    CU(cudaMalloc(&m->sg, sizeof(float) * (size_t)3 * m->h * B));
+    m->cap_xg = B;
   }
   if (B > m->cap_in) {
     CU(cudaStreamSynchronize(m->stream));
@@ -371,6 +384,7 @@ extern "C" void pg_free(pg_model* m) {
     for (size_t i = 0; i < g_groups.size(); ++i)
       if (g_groups[i].first == m) { free_group(g_groups[i].second); g_groups.erase(g_groups.begin() + i); break; }
   }
+  cudaFree(m->xg); cudaFree(m->sg);
   cudaFree(m->C); cudaFree(m->W1); cudaFree(m->W1T); cudaFree(m->b1); cudaFree(m->w2); cudaFree(m->b2);
   cudaFree(m->st); cudaFreeHost(m->st_host);
   if (m->copy_stream) cudaStreamSynchronize(m->copy_stream);
@@ -811,6 +825,11 @@ static pg_status run_step(pg_model* m, const int32_t* idx, const int32_t* corr, 
   if (m->comm) return dp_step(m, idx, corr, B, lr, loss_dev);
   const Geometry g = geometry(m, B);
   StepParams p = make_params(m, g, idx, corr, B, lr, loss_dev);
+  if (g.dw1_gemm) {   // the one-GPU step only (the data-parallel phases exchange records)
+    p.dw1_gemm = 1;
+    p.xg = m->xg;
+    p.sg = m->sg;
+  }
   int l = 0;
   launch_step(p, m->fused, m->fast, m->stream, &l);
   m->launches += l;

@@ -645,6 +645,7 @@ constexpr int kTTSmall = 4;
 constexpr int kTTMid = 8;
 template <int TT>
 __device__ void phase1_tiled_t(const StepParams& p, unsigned char* sm) {
+  constexpr bool kGemm = TT == kTTSmall;   // only the 4-example kernel carries the dW1-GEMM code
   constexpr int XTS = TT + 4;   // XT row stride (floats): TT examples + 4 pad, 16 B aligned
   const Layout& lay = p.lay;
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
@@ -760,6 +761,18 @@ __device__ void phase1_tiled_t(const StepParams& p, unsigned char* sm) {
     }
     __syncthreads();
     if (r < 2) trace_mark(p, 3 + 32 * r);
+    if (kGemm && p.dw1_gemm) {   // this chunk's inputs and deltas, example-major, for the phase-2 dW1 GEMM
+#pragma unroll 1
+      for (int t = tid; t < cnt * E * d; t += NT) {
+        const int e = t / (E * d), rw = t - e * (E * d);
+        p.xg[(size_t)(e0 + e) * E * d + rw] = XT[(size_t)rw * XTS + e];
+      }
+#pragma unroll 1
+      for (int t = tid; t < cnt * 3 * h; t += NT) {
+        const int e = t / (3 * h), rw = t - e * (3 * h);
+        p.sg[(size_t)(e0 + e) * 3 * h + rw] = SU[(size_t)rw * XTS + e];
+      }
+    }
     if (tid < h) {   // db1 / dw2 in example order
       for (int e = 0; e < cnt; ++e) { db1_acc += SE[(size_t)e * h + tid]; dw2_acc += DW[(size_t)e * h + tid]; }
     }
@@ -811,7 +824,7 @@ __device__ void phase1_tiled_t(const StepParams& p, unsigned char* sm) {
     // read (later chunks) and written as one coalesced 512 B access, with LA
     // record rows of reads in flight.  Centre rows add x'_c * delta' (delta'
     // read from shared memory) before their single write.
-    {
+    if (!(kGemm && p.dw1_gemm)) {
       const bool first = r == 0;
       const int u0 = 4 * lane;
       const bool has_u = u0 < h;
@@ -1051,8 +1064,117 @@ struct DenseSlice {
 };
 
 __device__ __forceinline__ DenseSlice dense_slice(const StepParams& p) {
-  const int NQ = (p.dense_len + 3) / 4, G = gridDim.x;
-  return {(int)((long long)blockIdx.x * NQ / G), (int)((long long)(blockIdx.x + 1) * NQ / G)};
+  // with dw1_gemm the records carry only db1 | dw2 (dW1 is the phase-2 GEMM)
+  const int Q0 = p.dw1_gemm ? (p.n * p.d * p.h) / 4 : 0;
+  const int NQ = (p.dense_len + 3) / 4 - Q0, G = gridDim.x;
+  return {Q0 + (int)((long long)blockIdx.x * NQ / G), Q0 + (int)((long long)(blockIdx.x + 1) * NQ / G)};
+}
+
+// dW1 as an output-tiled GEMM over the whole batch (p.dw1_gemm): CTA t takes
+// tiles of 16 dW1 rows (one slot, features j0..j0+15) x 32 hidden units and
+// stages the tile's inputs xg and deltas sg (example-major) in shared memory in
+// example chunks.  Thread (4 rows x 8 units, split s of 24) sums its examples
+// in order (register micro-tile: 3 LDS.128 per 32 FMA); the 24 splits are
+// combined in order, then W1 (and its transposed mirror) is updated.
+// dW1[slot p] = sum_e x_p sigma^T (context), x_c delta^T + x'_c delta'^T
+// (centre) -- the same terms as the per-CTA records, one fixed association.
+constexpr int kGRT = 16, kGCT = 32, kGEC = 256, kGNS = 24;
+__device__ void dw1_gemm_tiles(const StepParams& p, unsigned char* sm, bool write) {
+  constexpr int RT = kGRT, CT = kGCT, EC = kGEC, NS = kGNS;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int d = p.d, n = p.n, h = p.h, B = p.B, c = n >> 1, E = n + 1;
+  const int rtiles = n * d / RT, ctiles = h / CT, ntiles = rtiles * ctiles;
+  float* xs = reinterpret_cast<float*>(sm);              // [EC][2][RT]: x rows, x'_c rows
+  float* ss = xs + EC * 2 * RT;                          // [EC][2][CT]: class deltas, delta'
+  float* red = ss + EC * 2 * CT;                         // [NS][RT * CT]
+  const int mt = tid & 15, split = tid >> 4;             // micro-tile (rows 4 rt.., units 8 ct..)
+  const int rt = mt >> 2, ct = mt & 3;
+  #pragma unroll 1
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int tr = t / ctiles, tc = t - tr * ctiles;
+    const int row0 = tr * RT, sl = row0 / d, j0 = row0 - sl * d, col0 = tc * CT;
+    const bool centre = sl == c;
+    const int cls = centre ? 1 : 0;
+    // the tile's current W1 values, read now so the update at the end waits for nothing
+    float wcur[2];
+    #pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int o = tid + k * NT;
+      wcur[k] = o < RT * CT ? __ldcg(p.W1 + (size_t)(row0 + o / CT) * h + col0 + (o % CT)) : 0.f;
+    }
+    float acc[4][8];
+    #pragma unroll
+    for (int i = 0; i < 4; ++i)
+      #pragma unroll
+      for (int k = 0; k < 8; ++k) acc[i][k] = 0.f;
+    #pragma unroll 1
+    for (int eb = 0; eb < B; eb += EC) {
+      const int ne = min(EC, B - eb);
+      __syncthreads();   // the previous chunk's operands are consumed
+      // 16 B pieces: x (4 per row set), deltas (8 per set) per example
+      const int xq = RT / 4, sq = CT / 4, per_e = (centre ? 2 : 1) * (xq + sq);
+      for (int i = tid; i < ne * per_e; i += NT) {
+        const int e = i / per_e, k = i - e * per_e;
+        const size_t ge = (size_t)(eb + e);
+        const float* src;
+        float* dst;
+        if (k < xq) {
+          src = p.xg + (ge * E + sl) * d + j0 + 4 * k;                  dst = xs + (e * 2 + 0) * RT + 4 * k;
+        } else if (k < xq + sq) {
+          const int q = k - xq;
+          src = p.sg + (ge * 3 + cls) * h + col0 + 4 * q;              dst = ss + (e * 2 + 0) * CT + 4 * q;
+        } else if (k < 2 * xq + sq) {
+          const int q = k - xq - sq;
+          src = p.xg + (ge * E + n) * d + j0 + 4 * q;                   dst = xs + (e * 2 + 1) * RT + 4 * q;
+        } else {
+          const int q = k - 2 * xq - sq;
+          src = p.sg + (ge * 3 + 2) * h + col0 + 4 * q;                 dst = ss + (e * 2 + 1) * CT + 4 * q;
+        }
+        cp_async16(dst, src);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      if (t == blockIdx.x) trace_mark(p, 40 + 2 * (eb / EC));
+      if (split < NS) {
+        const int per = (ne + NS - 1) / NS, e0 = split * per, e1 = min(ne, e0 + per);
+        for (int k2 = 0; k2 < (centre ? 2 : 1); ++k2) {
+          #pragma unroll 2
+          for (int e = e0; e < e1; ++e) {
+            const float4 x = *reinterpret_cast<const float4*>(xs + (e * 2 + k2) * RT + 4 * rt);
+            const float4 s0 = *reinterpret_cast<const float4*>(ss + (e * 2 + k2) * CT + 8 * ct);
+            const float4 s1 = *reinterpret_cast<const float4*>(ss + (e * 2 + k2) * CT + 8 * ct + 4);
+            const float xv[4] = {x.x, x.y, x.z, x.w};
+            const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            #pragma unroll
+            for (int i = 0; i < 4; ++i)
+              #pragma unroll
+              for (int k = 0; k < 8; ++k) acc[i][k] = fmaf(xv[i], sv[k], acc[i][k]);
+          }
+        }
+      }
+    }
+    if (t == blockIdx.x) trace_mark(p, 46);
+    if (split < NS) {
+      #pragma unroll
+      for (int i = 0; i < 4; ++i)
+        #pragma unroll
+        for (int k = 0; k < 8; ++k) red[split * RT * CT + (4 * rt + i) * CT + 8 * ct + k] = acc[i][k];
+    }
+    __syncthreads();
+    if (t == blockIdx.x) trace_mark(p, 47);
+    #pragma unroll
+    for (int k = 0; k < 2; ++k) {   // splits combined in order; o = row * CT + unit
+      const int o = tid + k * NT;
+      if (o >= RT * CT || !write) continue;
+      float g = red[o];
+      #pragma unroll 4
+      for (int s2 = 1; s2 < NS; ++s2) g += red[s2 * RT * CT + o];
+      const int row = row0 + o / CT, col = col0 + (o % CT);
+      const float nw = wcur[k] - p.lr * g;
+      p.W1[(size_t)row * h + col] = nw;
+      if (p.W1T != nullptr) p.W1T[(size_t)col * (n * d) + row] = nw;
+    }
+  }
 }
 
 // Fixed-order reduction of quads [qb, qb+nq) over the P records: thread
@@ -1735,6 +1857,7 @@ __device__ void phase2_scatter_atomic(const StepParams& p) {
   }
 }
 
+template <bool kGemm>
 __device__ void phase2(const StepParams& p, unsigned char* sm) {
   __shared__ int s_flags;
   __shared__ float s_loss;
@@ -1842,6 +1965,12 @@ __device__ void phase2(const StepParams& p, unsigned char* sm) {
     else if (M > 0 && write) scatter_det_sorted(p, sm, ls);
   } else if (write) {
     phase2_scatter_atomic(p);
+  }
+  if (kGemm && p.dw1_gemm) {
+    __syncthreads();   // the merge's shared memory is free
+    trace_mark(p, 39);
+    dw1_gemm_tiles(p, sm, write);
+    trace_mark(p, 48);
   }
   if (tid == 0 && my_done == gridDim.x - 1) {   // every CTA has read this step's flags
     st->flags = 0;
@@ -2187,12 +2316,14 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p_in, int phase
       dp_merge(p, smem);
     }
   } else if (phases & 2) {
-    phase2(p, smem);
+    phase2<PATH == 3>(p, smem);
   }
   __syncthreads();
   trace_mark(p, 11);
   trace_clock(p, 13);
 }
+
+int step_dw1_gemm(int fast, int T) { return fast == 2 && T == kTTSmall; }
 
 int step_fast_ok(int d, int n, int h) {
   const int nw = (n + 1) * (d / 32);

@@ -154,6 +154,10 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.stagefb = o; o = align16(o + SB * d * 4);
   L.carry = o; o = align16(o + 2 * 4 * d * 4);   // [2][4 chains][d]
   o = o > fast_end ? o : fast_end;
+  if (fast == 2) {   // the phase-2 dW1 GEMM staging (step.cu dw1_gemm_tiles: RT 16, CT 32, EC 256, 24 splits)
+    const int gemm = 256 * 2 * (16 + 32) * 4 + 24 * 16 * 32 * 4;
+    o = o > gemm ? o : gemm;
+  }
   L.lbase = o; o = align16(o + (NLtot + 1) * 4);
   L.loff = o;  o = align16(o + (NLtot + 1) * 4);
   L.total2 = o;
@@ -215,6 +219,11 @@ struct StepParams {
   float* C;
   float* W1;
   float* W1T;        // tiled path: W1 transposed [h][n*d], kept in step by the dense update (else null)
+  // tiled path, small per-CTA batches (one GPU): dW1 as an output-tiled GEMM in
+  // phase 2 over the batch's inputs and deltas instead of per-CTA records
+  int dw1_gemm;
+  float* xg;         // [B][n+1][d]: example inputs per slot, slot n = corrupt centre
+  float* sg;         // [B][3][h]: sigma | delta | delta' per hidden unit
   float* b1;
   float* w2;
   const float* b2;
@@ -268,6 +277,7 @@ void launch_dp_table(const StepParams& p, float* table, int what, int num_sms, c
 int step_fast_ok(int d, int n, int h);
 int step_block_threads(int d, int n, int h, int fast);
 int step_chunk_T(int d, int n, int h, int fast, int per_cta);   // per_cta = ceil(B / P)
+int step_dw1_gemm(int fast, int T);   // 1: the tiled path takes dW1 as a phase-2 GEMM (small chunks)
 cudaError_t step_prepare(int fast, size_t optin, size_t* usable);
 
 }  // namespace pg

@@ -58,6 +58,15 @@ for k in order:
     if np.isnan(col).all():
         continue
     print(f"  {nm:9s} med {np.nanmedian(col) / 1e3:7.2f}  max {np.nanmean(np.nanmax(col, axis=1)) / 1e3:7.2f}")
+G = {39: "g.start", 40: "g.stage0", 42: "g.stage1", 44: "g.stage2", 46: "g.comp", 47: "g.red", 48: "g.end"}
+XG = tr.view(a.steps, 160, 64).cpu().numpy()[2:, :P].astype(np.float64)
+for k, nm in G.items():
+    col = XG[:, :, k]
+    t0 = XG[:, :, 0].min(axis=1, keepdims=True)
+    v = np.where(col > 0, col - t0, np.nan)
+    if np.isnan(v).all():
+        continue
+    print(f"  {nm:9s} med {np.nanmedian(v) / 1e3:7.2f}  max {np.nanmean(np.nanmax(v, axis=1)) / 1e3:7.2f}")
 
 # slowest CTAs (last step): end time, owner entry count M, per-stage deltas
 x = X[-1]
