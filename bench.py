@@ -350,7 +350,7 @@ def main():
                        "parallelism": f"dp{world}" if world > 1 else "single",
                        "scatter": args.scatter, "l2": "flushed (512 MB write) before every timed step",
                        "inputs": "Zipf(1) sliding windows + uniform corrupt centres, seed 42"},
-            "roofline": {"kernel": "pg::step_kernel<1> (fused cooperative step, h = 32 path)", "bound": "alu",
+            "roofline": {"kernel": "pg::step_kernel<5> (fused cooperative step, Polyglot-shape specialisation)", "bound": "alu",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": tr, "peak_source": f"FP32 FMA: 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz",
                          "flop_per_example": 2 * fma},
