@@ -684,6 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q = cols >> 2;
   const int G = q >= 32 ? 32 : q, per = 32 / G, sub = lane / G, gl = lane % G;
+  SORT_MARK(0);
   const int64_t ns = n < kHotSample ? n : kHotSample;
   // the sample: ns / 32 runs of 32 consecutive entries spread evenly over I
   // (one 128 B line per warp load: every CTA reads the same lines, so
@@ -728,6 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     }
   }
   // Everything up to grid_wait is CTA-local: it overlaps the barrier.
+  SORT_MARK(1);
   const unsigned long long target = grid_arrive(&st->hot_arrivals);
   // W's first touch by a reduction after a cold L2 is an L2 miss the atomic
   // unit waits on; when W is small next to the L2, pull it in while the
@@ -738,10 +740,12 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     for (int64_t l = (int64_t)blockIdx.x * kThreads + tid; l < lines; l += (int64_t)gridDim.x * kThreads)
       asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(wb + (l << 7)));
   }
+  SORT_MARK(9);
   for (int i = tid; i < kHotSampleHash; i += kThreads) { skey[i] = -1; scnt[i] = 0; }
   for (int i = tid; i < kHotHash; i += kThreads) hkey[i] = -1;
   if (tid == 0) ncand = 0;
   __syncthreads();
+  SORT_MARK(10);
 #pragma unroll
   for (int j = 0; j < kSPer; ++j) {
     const int row = samp[j];
@@ -755,6 +759,7 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     atomicAdd(&scnt[h], 1);
   }
   __syncthreads();
+  SORT_MARK(11);
   // candidates: rows seen >= kHotMin times (<= kHotSample / kHotMin = kHotCand
   // of them), ranked by (count desc, row asc) with a bitonic sort, so every
   // CTA derives the same ranking -- tier B's replica rows in global memory
@@ -784,6 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
         __syncthreads();
       }
   }
+  SORT_MARK(12);
   const int nh = nc < ha + hb ? nc : ha + hb;
   for (int a = tid; a < nh; a += kThreads) {
     const int r = (int)(unsigned)(cand[a] & 0xffffffffull);
@@ -816,7 +822,9 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   int64_t b0 = ((int64_t)blockIdx.x * NW + warp) * 32;
   const int64_t hi_all = n;
   int rl = b0 + lane < hi_all ? __ldg(I + b0 + lane) : -1;   // in flight across the barrier wait
+  SORT_MARK(2);
   grid_wait(&st->hot_arrivals, target);
+  SORT_MARK(3);
   if (blockIdx.x == 0 && tid == 0) { st->hot[par ^ 1].flag = 0; st->hot[par ^ 1].nbad = 0ull; }
   if (*(volatile const int*)&st->hot[par].flag) return;
   for (; b0 < hi_all; b0 += gstride) {
@@ -853,7 +861,9 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     }
     rl = rn;
   }
+  SORT_MARK(4);
   __syncthreads();
+  SORT_MARK(5);
   for (int t = tid; t < na * q; t += kThreads) {
     const int r = t / q, f = t - r * q;
     const float4* a = reinterpret_cast<const float4*>(accA) + (size_t)r * q + f;
@@ -864,10 +874,12 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     }
     red_add_v4(W + (size_t)hrow[r] * cols + 4 * f, sm4);
   }
+  SORT_MARK(6);
   if (nb == 0) return;   // identical in every CTA (same sample, same ranking)
   // tier B: after every CTA's reductions have landed, CTA c folds replica
   // rows j = c, c + grid, ... into W and clears them for the next call
   grid_barrier(&st->hot_arrivals);
+  SORT_MARK(7);
   for (int t = blockIdx.x * kThreads + tid; t < nb * q; t += gridDim.x * kThreads) {
     const int j = t / q, f = t - j * q;
     float4* r4 = reinterpret_cast<float4*>(rep + (size_t)j * kHotRep * cols) + f;
@@ -881,6 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     for (int r = 0; r < kHotRep; ++r) __stcg(r4 + (size_t)r * q, make_float4(0.f, 0.f, 0.f, 0.f));
     red_add_v4(W + (size_t)hrow[na + j] * cols + 4 * f, sm4);
   }
+  SORT_MARK(8);
 }
 
 // Lane group of G = cols/4 lanes (<= 32) per entry; 32/G entries per warp step.
