@@ -662,12 +662,27 @@ __global__ void sc_validate(const int32_t* __restrict__ I, int64_t n, int64_t ro
 constexpr int kHotSample = 4096;
 constexpr int kHotSampleHash = 8192;
 constexpr int kHotHash = 1024;
-constexpr int kHotB = 256;
+#ifndef PG_AH_HB
+#define PG_AH_HB 256
+#endif
+#ifndef PG_AH_REP
+#define PG_AH_REP 16
+#endif
+#ifndef PG_AH_HA
+#define PG_AH_HA 8
+#endif
+constexpr int kHotB = PG_AH_HB;
 constexpr int kHotMin = 4;                          // sample count of a hot row
 constexpr int kHotCand = 1024;   // power of two >= kHotSample / kHotMin: every row seen >= kHotMin times
 static_assert((kHotCand & (kHotCand - 1)) == 0 && kHotCand >= kHotSample / kHotMin, "candidate array");
-constexpr int kHotRep = 16;                         // replica rows per tier-B row
+constexpr int kHotRep = PG_AH_REP;                         // replica rows per tier-B row
 constexpr size_t kHotPrefetchMax = 48u << 20;
+#ifndef PG_AH_WPF
+#define PG_AH_WPF 2   // W into L2 before the stream: 0 none, 1 per-line prefetch, 2 bulk prefetch
+#endif
+#ifndef PG_AH_RANK
+#define PG_AH_RANK 1
+#endif
 template <int kThreads, int U>
 __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __restrict__ I,
                                                              const float* __restrict__ Y, float* W, int64_t rows,
@@ -733,12 +748,32 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   const unsigned long long target = grid_arrive(&st->hot_arrivals);
   // W's first touch by a reduction after a cold L2 is an L2 miss the atomic
   // unit waits on; when W is small next to the L2, pull it in while the
-  // prologue runs (this CTA's 1/gridDim share of its 128 B lines).
+  // prologue runs (this CTA's 1/gridDim share).
   if ((size_t)rows * cols * sizeof(float) <= kHotPrefetchMax) {
-    const int64_t lines = ((int64_t)rows * cols * (int64_t)sizeof(float)) >> 7;
+    const int64_t bytes = (int64_t)rows * cols * (int64_t)sizeof(float);
     const char* wb = reinterpret_cast<const char*>(W);
+#if PG_AH_WPF == 2
+    // bulk prefetches (16 B granular), one piece per lane of warp 0: a
+    // per-line prefetch loop put ~1350 instructions per SM into the LSU queue
+    // ahead of the prologue's shared-memory work
+    if (warp == 0) {
+      const int64_t slice = ((bytes / gridDim.x) + 15) & ~15ll, piece = ((slice / 32) + 15) & ~15ll;
+      const int64_t a = (int64_t)blockIdx.x * slice + lane * piece;
+      int64_t e = a + piece;
+      if (e > (int64_t)(blockIdx.x + 1) * slice) e = (int64_t)(blockIdx.x + 1) * slice;
+      if (e > (bytes & ~15ll)) e = bytes & ~15ll;
+      if (e > a) {
+        unsigned long long pol;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;"
+                     ::"l"(wb + a), "r"((unsigned)(e - a)), "l"(pol) : "memory");
+      }
+    }
+#elif PG_AH_WPF == 1
+    const int64_t lines = bytes >> 7;
     for (int64_t l = (int64_t)blockIdx.x * kThreads + tid; l < lines; l += (int64_t)gridDim.x * kThreads)
       asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(wb + (l << 7)));
+#endif
   }
   SORT_MARK(9);
   for (int i = tid; i < kHotSampleHash; i += kThreads) { skey[i] = -1; scnt[i] = 0; }
@@ -771,6 +806,25 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     }
   __syncthreads();
   const int nc = ncand;
+  const int nh = nc < ha + hb ? nc : ha + hb;
+#if PG_AH_RANK
+  // rank of candidate a = number of smaller keys (keys are distinct: one per
+  // row), counted against every candidate (broadcast smem reads) -- the order
+  // a sort would give, without its barriers
+  for (int a = tid; a < nc; a += kThreads) {
+    const unsigned long long key = cand[a];
+    int rk = 0;
+    for (int b = 0; b < nc; ++b) rk += cand[b] < key;
+    if (rk < nh) {
+      const int r = (int)(unsigned)(key & 0xffffffffull);
+      hrow[rk] = r;
+      unsigned h = ((unsigned)r * 2654435761u) & (kHotHash - 1);
+      while (atomicCAS(&hkey[h], -1, r) != -1) h = (h + 1) & (kHotHash - 1);
+      hslot[h] = rk;
+    }
+  }
+  SORT_MARK(12);
+#else
   int npow = 1;
   while (npow < nc) npow <<= 1;
   for (int i = nc + tid; i < npow; i += kThreads) cand[i] = ~0ull;
@@ -790,7 +844,6 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
       }
   }
   SORT_MARK(12);
-  const int nh = nc < ha + hb ? nc : ha + hb;
   for (int a = tid; a < nh; a += kThreads) {
     const int r = (int)(unsigned)(cand[a] & 0xffffffffull);
     hrow[a] = r;
@@ -798,6 +851,7 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
     while (atomicCAS(&hkey[h], -1, r) != -1) h = (h + 1) & (kHotHash - 1);
     hslot[h] = a;
   }
+#endif
   const int na = nh < ha ? nh : ha, nb = nh - na;
   __syncthreads();
   // tier A: [NW][na][q] private copies (dense for the rows actually taken)
@@ -876,11 +930,13 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   }
   SORT_MARK(6);
   if (nb == 0) return;   // identical in every CTA (same sample, same ranking)
-  // tier B: after every CTA's reductions have landed, CTA c folds replica
-  // rows j = c, c + grid, ... into W and clears them for the next call
+  // tier B: after every CTA's reductions have landed, the replica rows are
+  // folded into W and cleared for the next call
   grid_barrier(&st->hot_arrivals);
   SORT_MARK(7);
-  for (int t = blockIdx.x * kThreads + tid; t < nb * q; t += gridDim.x * kThreads) {
+  // items spread over every CTA (item t -> CTA t % grid): with t = CTA-major
+  // the 4096 items of 256 tier-B rows at d = 64 landed on 4 CTAs (~7 us tail)
+  for (int t = tid * gridDim.x + blockIdx.x; t < nb * q; t += gridDim.x * kThreads) {
     const int j = t / q, f = t - j * q;
     float4* r4 = reinterpret_cast<float4*>(rep + (size_t)j * kHotRep * cols) + f;
     float4 sm4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -951,7 +1007,7 @@ static void hot_tiers(int cols, int* ha, int* hb) {
   // at most 8 tier-A rows: the copies' shared memory shrinks the L1, which the
   // uniform case pays for (12 rows: 85.4 us, 8: 77.9 us L2-flushed) while the
   // Zipf case is no faster with more (88.1 us either way, scripts/ab_atomic.sh)
-  *ha = a > 8 ? 8 : a;
+  *ha = a > PG_AH_HA ? PG_AH_HA : a;
   (void)a;
   *hb = kHotB;   // tier B lives in global replica rows (ScatterPlan::off_rep)
 }
