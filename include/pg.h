@@ -139,9 +139,13 @@ pg_status pg_init(pg_model** out, int64_t vocab, int32_t dim, int32_t window,
 
 /* pg_train_step -- one SGD step on `batch` windows (the north-star
  * pg_train_step(idx_batch, corrupt_idx, lr) -> loss).
- *   loss_out: HOST pointer -> blocking: waits, reports device errors, writes L;
- *             DEVICE pointer -> asynchronous on the model stream; L (float) is
- *             written there when the step completes; errors are sticky;
+ *   loss_out: pageable HOST pointer -> blocking: waits, reports device errors,
+ *             writes L;
+ *             DEVICE pointer, or PAGE-LOCKED host pointer (cudaHostAlloc /
+ *             cudaHostRegister / torch pin_memory) -> asynchronous on the model
+ *             stream: the step kernel writes L (float) there itself (a 4-byte
+ *             device-to-host store for pinned memory), valid once the stream
+ *             has reached the step (pg_sync); errors are sticky;
  *             NULL -> asynchronous, loss discarded.
  * The returned loss is computed with the pre-step parameters.
  * After pg_attach_nccl, `batch` is this rank's shard (equal on all ranks), the

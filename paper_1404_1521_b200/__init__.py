@@ -197,7 +197,8 @@ def _check_batch(handle, idx_batch, corrupt_idx=None):
 
 def pg_train_step(handle, idx_batch, corrupt_idx, lr, loss_out=_HOST):
     """One SGD step.  loss_out="host" -> blocking, returns the float loss;
-    a device float32 tensor -> asynchronous, loss written there; None -> async."""
+    a device or pinned-host float32 tensor -> asynchronous, the step kernel
+    writes the loss there; None -> async (include/pg.h)."""
     batch = _check_batch(handle, idx_batch, corrupt_idx)
     # `is`, not `==`: comparing a torch tensor with a str costs ~13 us per call
     if loss_out is _HOST or (isinstance(loss_out, str) and loss_out == "host"):

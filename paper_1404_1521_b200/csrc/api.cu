@@ -168,13 +168,17 @@ __global__ void score_kernel(const float* __restrict__ C, const float* __restric
 // ------------------------------------------------------------------ helpers
 enum PtrKind { PTR_NULL, PTR_HOST, PTR_DEVICE };
 
-static PtrKind ptr_kind(const void* p) {
+// dev (optional): the device-side address of a page-locked host pointer (NULL
+// for pageable memory) -- the kernels can write such memory directly.
+static PtrKind ptr_kind(const void* p, void** dev = nullptr) {
+  if (dev) *dev = nullptr;
   if (!p) return PTR_NULL;
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return PTR_HOST;
   }
+  if (a.type == cudaMemoryTypeHost && dev) *dev = a.devicePointer;
   return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? PTR_DEVICE : PTR_HOST;
 }
 
@@ -563,12 +567,14 @@ extern "C" pg_status pg_train_step(pg_model* m, const int32_t* idx_batch, const 
   if (!std::isfinite(lr) || !(lr > 0.f)) return fail(PG_EINVAL, "pg_train_step: lr must be finite and > 0 (got %g)", lr);
   if (pg_status s = set_device(m)) return s;
   if (pg_status s = ensure_ws(m, batch, m->world)) return s;
-  const PtrKind kl = ptr_kind(loss_out);
+  void* pinned = nullptr;   // page-locked host loss_out: the step writes it through its device mapping
+  const PtrKind kl = ptr_kind(loss_out, &pinned);
   const int32_t *di = nullptr, *dc = nullptr;
   if (pg_status s = stage_inputs(m, idx_batch, corrupt_idx, batch, &di, &dc)) return s;
-  if (pg_status s = run_step(m, di, dc, batch, lr, kl == PTR_DEVICE ? loss_out : nullptr)) return s;
+  float* loss_dev = kl == PTR_DEVICE ? loss_out : static_cast<float*>(pinned);
+  if (pg_status s = run_step(m, di, dc, batch, lr, loss_dev)) return s;
   if (pg_status s = consume_inputs(m)) return s;
-  if (kl != PTR_HOST) return PG_OK;
+  if (kl != PTR_HOST || pinned) return PG_OK;
   CU(cudaMemcpyAsync(m->st_host, m->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
   *loss_out = m->st_host->last_loss;

@@ -283,6 +283,25 @@ def test_async_host_inputs_pipeline_equals_device_inputs(pg):
     a.close(); b.close()
 
 
+def test_pinned_host_loss_is_written_asynchronously(pg):
+    # a page-locked host loss_out makes the call asynchronous: the step kernel
+    # stores the loss through the buffer's device mapping (include/pg.h); after
+    # a sync the values equal the blocking call's, and the parameters match
+    import torch
+    batches = [synth.batch(POLY["V"], POLY["n"], 1024, seed=23, step=t) for t in range(6)]
+    a = make(pg, POLY, seed=9)
+    b = make(pg, POLY, seed=9)
+    ring = torch.full((6,), float("nan")).pin_memory()
+    for t, (i, c) in enumerate(batches):
+        a.train_step(torch.from_numpy(i).pin_memory(), torch.from_numpy(c).pin_memory(), 0.1, loss_out=ring[t:t + 1])
+    a.sync()
+    lb = [b.train_step(i, c, 0.1) for i, c in batches]
+    assert np.array_equal(ring.numpy(), np.array(lb, np.float32))
+    for x, y in zip(a.get_params()[:4], b.get_params()[:4]):
+        assert np.array_equal(x, y)
+    a.close(); b.close()
+
+
 def test_cuda_graph_capture_replay_equals_eager(pg):
     """PG_OPT_RESERVE pre-sizes the workspace so steps with device inputs and a
     device loss can be captured in a CUDA graph; replaying the graph must give
