@@ -1071,14 +1071,16 @@ __device__ __forceinline__ DenseSlice dense_slice(const StepParams& p) {
 }
 
 // dW1 as an output-tiled GEMM over the whole batch (p.dw1_gemm): CTA t takes
-// tiles of 16 dW1 rows (one slot, features j0..j0+15) x 32 hidden units and
-// stages the tile's inputs xg and deltas sg (example-major) in shared memory in
-// example chunks.  Thread (4 rows x 8 units, split s of 24) sums its examples
-// in order (register micro-tile: 3 LDS.128 per 32 FMA); the 24 splits are
-// combined in order, then W1 (and its transposed mirror) is updated.
+// tiles of kGRT dW1 rows (one slot) x kGCT hidden units and stages the tile's
+// inputs xg and deltas sg (example-major) in shared memory in example chunks.
+// Thread (4 rows x 8 units, split s of kGNS) sums its examples in order
+// (register micro-tile: 3 LDS.128 per 32 FMA); the splits are combined in
+// order, then W1 (and its transposed mirror) is updated.  16 x 32 tiles: the
+// large config (640 x 128) is 160 tiles, two on 12 of the 148 CTAs; 32 x 32
+// (80 tiles, one per CTA, 12 splits) measured slower (B = 512: 57.4 against
+// 53.3 us) -- a tile's time is its staging plus twice the per-thread sums.
 // dW1[slot p] = sum_e x_p sigma^T (context), x_c delta^T + x'_c delta'^T
 // (centre) -- the same terms as the per-CTA records, one fixed association.
-constexpr int kGRT = 16, kGCT = 32, kGEC = 256, kGNS = 24;
 __device__ void dw1_gemm_tiles(const StepParams& p, unsigned char* sm, bool write) {
   constexpr int RT = kGRT, CT = kGCT, EC = kGEC, NS = kGNS;
   const int tid = threadIdx.x, NT = blockDim.x;
@@ -1087,8 +1089,9 @@ __device__ void dw1_gemm_tiles(const StepParams& p, unsigned char* sm, bool writ
   float* xs = reinterpret_cast<float*>(sm);              // [EC][2][RT]: x rows, x'_c rows
   float* ss = xs + EC * 2 * RT;                          // [EC][2][CT]: class deltas, delta'
   float* red = ss + EC * 2 * CT;                         // [NS][RT * CT]
-  const int mt = tid & 15, split = tid >> 4;             // micro-tile (rows 4 rt.., units 8 ct..)
-  const int rt = mt >> 2, ct = mt & 3;
+  constexpr int MT = kGMT, CB = CT / 8, KO = (RT * CT + 383) / 384;
+  const int mt = tid % MT, split = tid / MT;             // micro-tile (rows 4 rt.., units 8 ct..)
+  const int rt = mt / CB, ct = mt - rt * CB;
   #pragma unroll 1
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int tr = t / ctiles, tc = t - tr * ctiles;
@@ -1096,9 +1099,9 @@ __device__ void dw1_gemm_tiles(const StepParams& p, unsigned char* sm, bool writ
     const bool centre = sl == c;
     const int cls = centre ? 1 : 0;
     // the tile's current W1 values, read now so the update at the end waits for nothing
-    float wcur[2];
+    float wcur[KO];
     #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < KO; ++k) {
       const int o = tid + k * NT;
       wcur[k] = o < RT * CT ? __ldcg(p.W1 + (size_t)(row0 + o / CT) * h + col0 + (o % CT)) : 0.f;
     }
@@ -1163,7 +1166,7 @@ __device__ void dw1_gemm_tiles(const StepParams& p, unsigned char* sm, bool writ
     __syncthreads();
     if (t == blockIdx.x) trace_mark(p, 47);
     #pragma unroll
-    for (int k = 0; k < 2; ++k) {   // splits combined in order; o = row * CT + unit
+    for (int k = 0; k < KO; ++k) {   // splits combined in order; o = row * CT + unit
       const int o = tid + k * NT;
       if (o >= RT * CT || !write) continue;
       float g = red[o];

@@ -42,6 +42,18 @@ struct DevStatus {
 static_assert(sizeof(DevStatus) == 3 * 128 + 160 * 8, "DevStatus layout");
 
 // Shared-memory carve-up (byte offsets), computed once on the host.
+// phase-2 dW1 GEMM of the tiled path (step.cu dw1_gemm_tiles): RT x CT output
+// tiles, EC examples staged per pass, 4 x 8 register micro-tiles, the 384
+// threads split into kGNS example ranges
+#ifndef PG_G_RT
+#define PG_G_RT 16
+#endif
+#ifndef PG_G_CT
+#define PG_G_CT 32
+#endif
+constexpr int kGRT = PG_G_RT, kGCT = PG_G_CT, kGEC = 256;
+constexpr int kGMT = (kGRT / 4) * (kGCT / 8), kGNS = 384 / kGMT;
+
 struct Layout {
   // phase 1
   int xs, pg, sig, gz, hinge, rows, ws, red, wsm;
@@ -154,8 +166,8 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.stagefb = o; o = align16(o + SB * d * 4);
   L.carry = o; o = align16(o + 2 * 4 * d * 4);   // [2][4 chains][d]
   o = o > fast_end ? o : fast_end;
-  if (fast == 2) {   // the phase-2 dW1 GEMM staging (step.cu dw1_gemm_tiles: RT 16, CT 32, EC 256, 24 splits)
-    const int gemm = 256 * 2 * (16 + 32) * 4 + 24 * 16 * 32 * 4;
+  if (fast == 2) {   // the phase-2 dW1 GEMM staging (step.cu dw1_gemm_tiles)
+    const int gemm = kGEC * 2 * (kGRT + kGCT) * 4 + kGNS * kGRT * kGCT * 4;
     o = o > gemm ? o : gemm;
   }
   L.lbase = o; o = align16(o + (NLtot + 1) * 4);
