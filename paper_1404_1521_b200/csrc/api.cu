@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -230,7 +231,10 @@ struct Geometry {
 
 static Geometry geometry(const pg_model* m, int B, int world = 1) {
   Geometry g{};
-  g.P = B < m->num_sms ? B : m->num_sms;
+  // PG_STEP_CTAS caps the CTAs per step (experiments; default: one per SM)
+  static const int cap = getenv("PG_STEP_CTAS") ? atoi(getenv("PG_STEP_CTAS")) : 0;
+  const int P = cap > 0 && cap < m->num_sms ? cap : m->num_sms;
+  g.P = B < P ? B : P;
   const int per = (B + g.P - 1) / g.P;
   g.T = step_chunk_T(m->d, m->n, m->h, m->fast, per);
   g.R = (per + g.T - 1) / g.T;

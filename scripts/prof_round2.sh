@@ -7,7 +7,8 @@ bench)
   python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
   python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_r2.csv python bench.py --steps 10 --warmup 3 --no-extras --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1
-  for tool in memcheck racecheck synccheck; do compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_run.py > gpurun_out/sanitize_$tool.log 2>&1; done
+  # compute-sanitizer runs (profiles/sanitizer_r2) are no longer possible: the
+  # pool closed the tool after it left GPUs needing a reset
   ;;
 step)
   ncu --set full --import-source on --clock-control none -k regex:step_kernel -s 3 -c 1 -o gpurun_out/step_b4096_r2 python scripts/prof_step.py --batch 4096 > gpurun_out/ncu_step.log 2>&1
