@@ -21,6 +21,8 @@
 // Latency structure (the step is latency-bound below B ~ 8k): every global
 // round trip is issued for a whole chunk at once -- cp.async for the row
 // gather, unrolled loads for W1, the dense partials and the owner lists.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "step.cuh"
 
@@ -2280,6 +2282,9 @@ __global__ void dp_table_apply_kernel(StepParams p, float* table, int zero) {
 template <int PATH, int DP, int ACT>
 __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p_in, int phases) {
   extern __shared__ __align__(16) unsigned char smem[];
+  // under PG_PDL=1 (launch_step_phases) the kernel may be placed before the
+  // previous one has completed: nothing is read or written before it has
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   StepParams p = p_in;
   p.act = ACT;
   if (PATH == 5) {
@@ -2311,6 +2316,7 @@ __global__ void __launch_bounds__(384, 1) step_kernel(StepParams p_in, int phase
     __syncthreads();
   }
   trace_mark(p, 7);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the next step may begin its launch
   if (DP) {
     if (phases & 8) dp_publish(p, smem);
     if (phases & 16) {
@@ -2395,13 +2401,40 @@ cudaError_t step_prepare(int fast, size_t optin, size_t* usable) {
   return cudaSuccess;
 }
 
+// Launch: the in-kernel grid barrier needs every CTA resident at once.  The
+// default is a cooperative launch (the runtime co-schedules the grid even
+// next to other work).  PG_PDL=1 selects a plain launch with programmatic
+// stream serialisation instead: the kernel's first instruction is
+// griddepcontrol.wait, so it reads nothing before the previous kernel on the
+// stream has completed, but its CTAs are placed while the previous step drains
+// (back-to-back steps: 2.5 -> 0.65 us between kernels, scripts/micro/launch_gap.cu;
+// device-fed back-to-back Polyglot B = 4096 steps 28.4 -> 26.5 us; a
+// cooperative launch does not overlap).  Co-residency is then by construction
+// (P <= #SMs CTAs, one fits per SM), which holds only while no kernel that
+// waits on this one occupies SMs concurrently -- hence opt-in.
 void launch_step_phases(const StepParams& p, int phases, int fast, cudaStream_t s, int* launches) {
   const int NT = step_block_threads(p.d, p.n, p.h, fast);
   const bool poly = fast == 1 && poly_shape(p.d, p.n, p.h) && p.T == kTMax && NT == 384;
   const void* fn = step_fn(fast, p.T, (phases & 24) != 0, p.act, poly);
   void* args[] = {(void*)&p, (void*)&phases};
-  if ((phases & 1) && (phases & 10)) cudaLaunchCooperativeKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
-  else cudaLaunchKernel(fn, dim3(p.P), dim3(NT), args, (size_t)p.smem_bytes, s);
+  static const int pdl = getenv("PG_PDL") ? atoi(getenv("PG_PDL")) : 0;
+  const bool grid_sync = (phases & 1) && (phases & 10);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.P);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = (size_t)p.smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  if (pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+  } else {
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = grid_sync || pdl ? 1 : 0;
+  cudaLaunchKernelExC(&cfg, fn, args);
   *launches += 1;
 }
 

@@ -362,3 +362,42 @@ def test_nonfinite_loss_diverged_no_mutation(pg, scatter, fused):
     m.set_params(C, W1, b1, w2, b2)
     m.train_step(idx, corr, 0.1)   # and the model keeps working
     m.close()
+
+
+_PDL_SCRIPT = r"""
+import sys, hashlib
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+import paper_1404_1521_b200 as pg, synth
+m = pg.PolyglotModel(100_000, 64, 5, 32, seed=3)
+bs = [synth.batch(100_000, 5, 2048, seed=31, step=t) for t in range(8)]
+di = [torch.from_numpy(i).cuda() for i, _ in bs]
+dc = [torch.from_numpy(c).cuda() for _, c in bs]
+loss = torch.zeros(8, device="cuda")
+for t in range(8):
+    m.train_step(di[t], dc[t], 0.5, loss_out=loss[t:t + 1])   # back to back, no host sync
+m.sync()
+h = hashlib.sha256(loss.cpu().numpy().tobytes())
+for x in m.get_params()[:4]:
+    h.update(np.ascontiguousarray(x).tobytes())
+print(h.hexdigest())
+"""
+
+
+@pytest.mark.parametrize("pdl", ["0", "1"])
+def test_pdl_launch_matches_cooperative_bitwise(pg, pdl):
+    # PG_PDL=1 launches the step without the cooperative attribute, with
+    # programmatic stream serialisation (step.cu launch_step_phases): eight
+    # back-to-back DET steps must give the bits of the default launch
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for v in ("0", pdl):
+        env = dict(os.environ, PG_PDL=v)
+        r = subprocess.run([sys.executable, "-c", _PDL_SCRIPT, root], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[v] = r.stdout.strip().splitlines()[-1]
+    assert out["0"] == out[pdl]
