@@ -992,7 +992,7 @@ __global__ void sc_atomic_scalar(const int32_t* __restrict__ I, const float* __r
 // 4 rows in flight per lane group; 512-thread variants measured 20-30 % slower.
 // sc_atomic_hot launch shape: 1024 threads (32 warps, the most at 64 registers)
 // with 4 rows in flight per lane group; measured slower: 1024 x 2 / x 8 rows,
-// 768 x 8, 512 x 8 (scripts/ab_atomic.sh history in DESIGN.md 7.2).
+// 768 x 8, 512 x 8 (history in DESIGN.md 7.2).
 constexpr int kHotThreads = 1024;
 static const void* const kHotFn = (const void*)sc_atomic_hot<kHotThreads, 4>;
 constexpr size_t kHotSmemMax = 200 * 1024;
@@ -1006,7 +1006,7 @@ static void hot_tiers(int cols, int* ha, int* hb) {
   int a = (int)(kHotSmemMax / ((size_t)hot_copies(cols) * row));
   // at most 8 tier-A rows: the copies' shared memory shrinks the L1, which the
   // uniform case pays for (12 rows: 85.4 us, 8: 77.9 us L2-flushed) while the
-  // Zipf case is no faster with more (88.1 us either way, scripts/ab_atomic.sh)
+  // Zipf case is no faster with more (88.1 us either way)
   *ha = a > PG_AH_HA ? PG_AH_HA : a;
   (void)a;
   *hb = kHotB;   // tier B lives in global replica rows (ScatterPlan::off_rep)

@@ -1,5 +1,8 @@
+"""Host-side cost per pg_train_step call (device / pinned inputs, device loss) against the
+GPU step time, and the bare ctypes call floor."""
 import sys, time
-sys.path.insert(0, "/root/repo")
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, numpy as np
 import paper_1404_1521_b200 as pg, synth
 V, d, n, h = 100_000, 64, 5, 32
