@@ -233,16 +233,17 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    with torch.cuda.stream(stream):
-        for t in range(args.warmup):
-            model.train_step(d_idx[t], d_corr[t], args.lr, loss_out=loss_dev)
-    barrier()
-    model.sync()
-    l0 = model.kernel_launches()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         barrier()
         with torch.cuda.stream(stream):
+            # the W warm-up steps run exactly like the timed ones (flush, step)
+            # and straight before them, with no host sync in between: after an
+            # idle GPU the first step measured ~55 us instead of ~31
+            for t in range(args.warmup):
+                flush.zero_()
+                model.train_step(d_idx[t], d_corr[t], args.lr, loss_out=loss_dev)
+            l0 = model.kernel_launches()
             for k in range(args.steps):
                 flush.zero_()                      # L2 flush, outside the timed region
                 ev[k][0].record(stream)
@@ -265,7 +266,8 @@ def main():
     ms_per_step = tot_ms / args.steps
     value = B * world * args.steps / (tot_ms / 1e3)
     step_stats = {"median_ms": statistics.median(times), "min_ms": min(times), "max_ms": max(times),
-                  "pstdev_ms": statistics.pstdev(times), "rank": rank}   # this rank's K event-timed steps
+                  "pstdev_ms": statistics.pstdev(times), "rank": rank,   # this rank's K event-timed steps
+                  "argmax": max(range(len(times)), key=lambda i: times[i])}
 
     # ---- warm-L2 steady state: K steps back to back (table stays L2-resident)
     with torch.cuda.stream(stream):
