@@ -3,6 +3,8 @@
 // Owns device memory, the model stream, lazily sized per-batch workspace and
 // the launches of the sm_100a kernels (step.cu, scatter.cu, and the init and
 // score kernels below).  No torch types cross this boundary.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -57,6 +59,8 @@ struct pg_model {
   float* xg = nullptr;    // tiled path, small chunks: [B][n+1][d] inputs for the phase-2 dW1 GEMM
   float* sg = nullptr;    //   and [B][3][h] deltas
   int64_t cap_xg = 0;     //   examples they hold
+  void* d_tmap = nullptr; //   TMA tensor maps over xg / sg for the dW1 GEMM (2 x 128 B)
+  int tmap_B = 0;         //   the batch they were encoded for
   DevStatus* st = nullptr;
   DevStatus* st_host = nullptr;  // pinned mirror for blocking reads
   cudaStream_t stream = nullptr;
@@ -249,6 +253,46 @@ static Geometry geometry(const pg_model* m, int B, int world = 1) {
   return g;
 }
 
+// TMA tensor maps of the dW1 GEMM operands (step.cu dw1_gemm_tiles): xg as a
+// 3-D tensor (d, n+1, B) with boxes (kGRT, 1, kGEC), sg as (h, 3, B) with boxes
+// (kGCT, 1, kGEC); fp32, no swizzle, out-of-range examples read as zeros.  The
+// driver's encoder is reached through the runtime (no -lcuda).
+static pg_status encode_tmaps(pg_model* m, int B) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(PG_ECUDA, "cuTensorMapEncodeTiled is not available");
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  alignas(64) CUtensorMap maps[2];
+  const cuuint32_t one[3] = {1, 1, 1};
+  {
+    const cuuint64_t dim[3] = {(cuuint64_t)m->d, (cuuint64_t)(m->n + 1), (cuuint64_t)B};
+    const cuuint64_t stride[2] = {sizeof(float) * (cuuint64_t)m->d, sizeof(float) * (cuuint64_t)m->d * (m->n + 1)};
+    const cuuint32_t box[3] = {(cuuint32_t)kGRT, 1, (cuuint32_t)kGEC};
+    if (enc(&maps[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, m->xg, dim, stride, box, one, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(PG_ECUDA, "tensor map of the GEMM inputs could not be encoded");
+  }
+  {
+    const cuuint64_t dim[3] = {(cuuint64_t)m->h, 3, (cuuint64_t)B};
+    const cuuint64_t stride[2] = {sizeof(float) * (cuuint64_t)m->h, sizeof(float) * (cuuint64_t)m->h * 3};
+    const cuuint32_t box[3] = {(cuuint32_t)kGCT, 1, (cuuint32_t)kGEC};
+    if (enc(&maps[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, m->sg, dim, stride, box, one, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(PG_ECUDA, "tensor map of the GEMM deltas could not be encoded");
+  }
+  if (!m->d_tmap) CU(cudaMalloc(&m->d_tmap, sizeof(maps)));
+  // ordered on the model stream before the next step; the source is copied
+  // out before cudaMemcpyAsync returns (pageable memory)
+  CU(cudaMemcpyAsync(m->d_tmap, maps, sizeof(maps), cudaMemcpyHostToDevice, m->stream));
+  m->tmap_B = B;
+  return PG_OK;
+}
+
 static pg_status ensure_ws(pg_model* m, int B, int world = 1) {
   Geometry g = geometry(m, B, world);
   if (g.smem > m->smem_max)
@@ -273,6 +317,10 @@ static pg_status ensure_ws(pg_model* m, int B, int world = 1) {
     CU(cudaMalloc(&m->xg, sizeof(float) * (size_t)(m->n + 1) * m->d * B));
     CU(cudaMalloc(&m->sg, sizeof(float) * (size_t)3 * m->h * B));
     m->cap_xg = B;
+    m->tmap_B = 0;
+  }
+  if (g.dw1_gemm && B != m->tmap_B) {   // (re-)encode the tensor maps for this batch
+    if (pg_status s = encode_tmaps(m, B)) return s;
   }
   if (B > m->cap_in) {
     CU(cudaStreamSynchronize(m->stream));
@@ -392,7 +440,7 @@ extern "C" void pg_free(pg_model* m) {
     for (size_t i = 0; i < g_groups.size(); ++i)
       if (g_groups[i].first == m) { free_group(g_groups[i].second); g_groups.erase(g_groups.begin() + i); break; }
   }
-  cudaFree(m->xg); cudaFree(m->sg);
+  cudaFree(m->xg); cudaFree(m->sg); cudaFree(m->d_tmap);
   cudaFree(m->C); cudaFree(m->W1); cudaFree(m->W1T); cudaFree(m->b1); cudaFree(m->w2); cudaFree(m->b2);
   cudaFree(m->st); cudaFreeHost(m->st_host);
   if (m->copy_stream) cudaStreamSynchronize(m->copy_stream);
@@ -839,6 +887,7 @@ static pg_status run_step(pg_model* m, const int32_t* idx, const int32_t* corr, 
     p.dw1_gemm = 1;
     p.xg = m->xg;
     p.sg = m->sg;
+    p.tmap = m->d_tmap;
   }
   int l = 0;
   launch_step(p, m->fused, m->fast, m->stream, &l);

@@ -1083,23 +1083,62 @@ __device__ __forceinline__ DenseSlice dense_slice(const StepParams& p) {
 // 53.3 us) -- a tile's time is its staging plus twice the per-thread sums.
 // dW1[slot p] = sum_e x_p sigma^T (context), x_c delta^T + x'_c delta'^T
 // (centre) -- the same terms as the per-CTA records, one fixed association.
+__device__ __forceinline__ unsigned smem_u32(const void* q) { return (unsigned)__cvta_generic_to_shared(q); }
+// One 3-D tensor tile (TMA, cp.async.bulk.tensor) into shared memory, completing on `bar`.
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, unsigned long long* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
+
 __device__ void dw1_gemm_tiles(const StepParams& p, unsigned char* sm, bool write) {
   constexpr int RT = kGRT, CT = kGCT, EC = kGEC, NS = kGNS;
   const int tid = threadIdx.x, NT = blockDim.x;
-  const int d = p.d, n = p.n, h = p.h, B = p.B, c = n >> 1, E = n + 1;
+  const int d = p.d, n = p.n, h = p.h, B = p.B, c = n >> 1;
   const int rtiles = n * d / RT, ctiles = h / CT, ntiles = rtiles * ctiles;
-  float* xs = reinterpret_cast<float*>(sm);              // [EC][2][RT]: x rows, x'_c rows
-  float* ss = xs + EC * 2 * RT;                          // [EC][2][CT]: class deltas, delta'
-  float* red = ss + EC * 2 * CT;                         // [NS][RT * CT]
+  // operands staged by TMA (tensor maps over xg / sg, built on the host): one
+  // box per operand and pass of EC examples, example-major -- [EC][RT] x rows
+  // of the tile's slot (and of the corrupt centre for the centre slot),
+  // [EC][CT] deltas; examples past B arrive as zeros.  A ring of kGBUF pass
+  // buffers: a tile's first kGBUF passes are all issued at once (B <= 512
+  // is one TMA round trip), later passes refill the buffer just consumed.
+  constexpr int NB = kGBUF, BUF = 2 * EC * (RT + CT);    // floats per buffer
+  unsigned char* base = sm + ((128u - (smem_u32(sm) & 127u)) & 127u);
+  float* bufs = reinterpret_cast<float*>(base);          // [NB][xs0 | xs1 | ss0 | ss1]
+  float* red = bufs;                                     // [NS][RT * CT], after a tile's last pass
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(bufs + NB * BUF);   // [NB]
+  const unsigned char* tmx = reinterpret_cast<const unsigned char*>(p.tmap);
+  const unsigned char* tms = tmx + 128;
+  if (tid < NB) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar + tid)) : "memory");
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  unsigned qn = 0;   // passes issued before this tile: pass q uses buffer q % NB, phase (q / NB) & 1
   constexpr int MT = kGMT, CB = CT / 8, KO = (RT * CT + 383) / 384;
   const int mt = tid % MT, split = tid / MT;             // micro-tile (rows 4 rt.., units 8 ct..)
   const int rt = mt / CB, ct = mt - rt * CB;
+  const int npass = (B + EC - 1) / EC;
   #pragma unroll 1
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int tr = t / ctiles, tc = t - tr * ctiles;
     const int row0 = tr * RT, sl = row0 / d, j0 = row0 - sl * d, col0 = tc * CT;
     const bool centre = sl == c;
     const int cls = centre ? 1 : 0;
+    auto issue = [&](unsigned q, int eb) {   // thread 0: the pass at example eb into buffer q % NB
+      float* xb = bufs + (q % NB) * BUF;
+      unsigned long long* br = bar + (q % NB);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic accesses before the async writes
+      const unsigned bytes = (unsigned)((centre ? 2 : 1) * EC * (RT + CT) * sizeof(float));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(br)), "r"(bytes) : "memory");
+      tma_load_3d(xb, tmx, br, j0, sl, eb);
+      tma_load_3d(xb + 2 * EC * RT, tms, br, col0, cls, eb);
+      if (centre) {
+        tma_load_3d(xb + EC * RT, tmx, br, j0, n, eb);
+        tma_load_3d(xb + 2 * EC * RT + EC * CT, tms, br, col0, 2, eb);
+      }
+    };
+    __syncthreads();   // the ring is free (the previous tile's split sums are read)
+    if (tid == 0)
+      for (int k = 0; k < NB && k < npass; ++k) issue(qn + k, k * EC);
     // the tile's current W1 values, read now so the update at the end waits for nothing
     float wcur[KO];
     #pragma unroll
@@ -1107,63 +1146,54 @@ __device__ void dw1_gemm_tiles(const StepParams& p, unsigned char* sm, bool writ
       const int o = tid + k * NT;
       wcur[k] = o < RT * CT ? __ldcg(p.W1 + (size_t)(row0 + o / CT) * h + col0 + (o % CT)) : 0.f;
     }
-    float acc[4][8];
+    float2 acc[4][4];   // (unit 2k, 2k+1) pairs: one FFMA2 per pair, the same per-unit rounding as FFMA
     #pragma unroll
     for (int i = 0; i < 4; ++i)
       #pragma unroll
-      for (int k = 0; k < 8; ++k) acc[i][k] = 0.f;
+      for (int k = 0; k < 4; ++k) acc[i][k] = make_float2(0.f, 0.f);
     #pragma unroll 1
-    for (int eb = 0; eb < B; eb += EC) {
-      const int ne = min(EC, B - eb);
-      __syncthreads();   // the previous chunk's operands are consumed
-      // 16 B pieces: x (4 per row set), deltas (8 per set) per example
-      const int xq = RT / 4, sq = CT / 4, per_e = (centre ? 2 : 1) * (xq + sq);
-      for (int i = tid; i < ne * per_e; i += NT) {
-        const int e = i / per_e, k = i - e * per_e;
-        const size_t ge = (size_t)(eb + e);
-        const float* src;
-        float* dst;
-        if (k < xq) {
-          src = p.xg + (ge * E + sl) * d + j0 + 4 * k;                  dst = xs + (e * 2 + 0) * RT + 4 * k;
-        } else if (k < xq + sq) {
-          const int q = k - xq;
-          src = p.sg + (ge * 3 + cls) * h + col0 + 4 * q;              dst = ss + (e * 2 + 0) * CT + 4 * q;
-        } else if (k < 2 * xq + sq) {
-          const int q = k - xq - sq;
-          src = p.xg + (ge * E + n) * d + j0 + 4 * q;                   dst = xs + (e * 2 + 1) * RT + 4 * q;
-        } else {
-          const int q = k - 2 * xq - sq;
-          src = p.sg + (ge * 3 + 2) * h + col0 + 4 * q;                 dst = ss + (e * 2 + 1) * CT + 4 * q;
-        }
-        cp_async16(dst, src);
-      }
-      cp_async_wait_all();
-      __syncthreads();
-      if (t == blockIdx.x) trace_mark(p, 40 + 2 * (eb / EC));
+    for (int ip = 0; ip < npass; ++ip) {
+      const unsigned q = qn + ip;
+      const int eb = ip * EC, ne = min(EC, B - eb);
+      asm volatile(
+          "{\n .reg .pred P1;\n WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @!P1 bra WAIT_%=;\n}\n"
+          ::"r"(smem_u32(bar + (q % NB))), "r"((q / NB) & 1u) : "memory");
+      if (t == blockIdx.x && ip < 2) trace_mark(p, 40 + 2 * ip);
       if (split < NS) {
+        const float* xb = bufs + (q % NB) * BUF;
         const int per = (ne + NS - 1) / NS, e0 = split * per, e1 = min(ne, e0 + per);
         for (int k2 = 0; k2 < (centre ? 2 : 1); ++k2) {
+          const float* xk = xb + k2 * EC * RT;
+          const float* sk = xb + 2 * EC * RT + k2 * EC * CT;
           #pragma unroll 2
           for (int e = e0; e < e1; ++e) {
-            const float4 x = *reinterpret_cast<const float4*>(xs + (e * 2 + k2) * RT + 4 * rt);
-            const float4 s0 = *reinterpret_cast<const float4*>(ss + (e * 2 + k2) * CT + 8 * ct);
-            const float4 s1 = *reinterpret_cast<const float4*>(ss + (e * 2 + k2) * CT + 8 * ct + 4);
+            const float4 x = *reinterpret_cast<const float4*>(xk + e * RT + 4 * rt);
+            const float4 s0 = *reinterpret_cast<const float4*>(sk + e * CT + 8 * ct);
+            const float4 s1 = *reinterpret_cast<const float4*>(sk + e * CT + 8 * ct + 4);
             const float xv[4] = {x.x, x.y, x.z, x.w};
-            const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            const float2 sv[4] = {make_float2(s0.x, s0.y), make_float2(s0.z, s0.w), make_float2(s1.x, s1.y),
+                                  make_float2(s1.z, s1.w)};
             #pragma unroll
             for (int i = 0; i < 4; ++i)
               #pragma unroll
-              for (int k = 0; k < 8; ++k) acc[i][k] = fmaf(xv[i], sv[k], acc[i][k]);
+              for (int k = 0; k < 4; ++k) acc[i][k] = __ffma2_rn(make_float2(xv[i], xv[i]), sv[k], acc[i][k]);
           }
         }
       }
+      if (ip + NB < npass) {   // refill the buffer just consumed
+        __syncthreads();
+        if (tid == 0) issue(q + NB, (ip + NB) * EC);
+      }
     }
+    qn += npass;
+    __syncthreads();   // every pass is consumed: the split sums take the ring
     if (t == blockIdx.x) trace_mark(p, 46);
     if (split < NS) {
       #pragma unroll
       for (int i = 0; i < 4; ++i)
         #pragma unroll
-        for (int k = 0; k < 8; ++k) red[split * RT * CT + (4 * rt + i) * CT + 8 * ct + k] = acc[i][k];
+        for (int k = 0; k < 4; ++k)
+          *reinterpret_cast<float2*>(red + split * RT * CT + (4 * rt + i) * CT + 8 * ct + 2 * k) = acc[i][k];
     }
     __syncthreads();
     if (t == blockIdx.x) trace_mark(p, 47);

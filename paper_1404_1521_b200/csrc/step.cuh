@@ -51,8 +51,9 @@ static_assert(sizeof(DevStatus) == 3 * 128 + 160 * 8, "DevStatus layout");
 #ifndef PG_G_CT
 #define PG_G_CT 32
 #endif
-constexpr int kGRT = PG_G_RT, kGCT = PG_G_CT, kGEC = 256;
+constexpr int kGRT = PG_G_RT, kGCT = PG_G_CT, kGEC = 128, kGBUF = 4;   // EC examples per pass, kGBUF passes in flight (TMA)
 constexpr int kGMT = (kGRT / 4) * (kGCT / 8), kGNS = 384 / kGMT;
+static_assert(kGNS * kGRT * kGCT <= kGBUF * kGEC * 2 * (kGRT + kGCT), "split sums fit the pass buffers");
 
 struct Layout {
   // phase 1
@@ -167,7 +168,7 @@ __host__ __device__ inline Layout make_layout(int d, int n, int h, int T, int NT
   L.carry = o; o = align16(o + 2 * 4 * d * 4);   // [2][4 chains][d]
   o = o > fast_end ? o : fast_end;
   if (fast == 2) {   // the phase-2 dW1 GEMM staging (step.cu dw1_gemm_tiles)
-    const int gemm = kGEC * 2 * (kGRT + kGCT) * 4 + kGNS * kGRT * kGCT * 4;
+    const int gemm = kGBUF * kGEC * 2 * (kGRT + kGCT) * 4 + 256;   // pass buffers (the split sums alias them) + mbarriers, 128 B alignment
     o = o > gemm ? o : gemm;
   }
   L.lbase = o; o = align16(o + (NLtot + 1) * 4);
@@ -236,6 +237,7 @@ struct StepParams {
   int dw1_gemm;
   float* xg;         // [B][n+1][d]: example inputs per slot, slot n = corrupt centre
   float* sg;         // [B][3][h]: sigma | delta | delta' per hidden unit
+  const void* tmap;  // two CUtensorMaps (128 B each, device memory): xg as (d, n+1, B), sg as (h, 3, B)
   float* b1;
   float* w2;
   const float* b2;
