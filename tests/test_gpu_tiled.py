@@ -26,9 +26,11 @@ def pg():
 
 
 @pytest.mark.parametrize("cfg", SHAPES, ids=lambda c: f"d{c['d']}n{c['n']}h{c['h']}")
-@pytest.mark.parametrize("B", [5, 300, 1000, 2400 + 13])   # 4-, 4-, 8- and 16-example chunks
+@pytest.mark.parametrize("B", [5, 300, 580, 1000, 2400 + 13])   # 4-, 4-, 4-, 8- and 16-example chunks
 def test_tiled_parity(pg, cfg, B):
-    # B = 2413 > 148 * 16: several 16-example chunks per CTA (record RMW path)
+    # B = 580: the dW1 GEMM's 5 passes of 128 examples refill its 4-buffer TMA
+    # ring mid-tile; B = 2413 > 148 * 16: several 16-example chunks per CTA
+    # (record RMW path)
     m = pg.PolyglotModel(cfg["V"], cfg["d"], cfg["n"], cfg["h"], seed=11)
     gl, rl, p0, pend, ref = run_both(m, **cfg, B=B, steps=3, kind="iid" if B < 100 else "sliding")
     assert_parity(gl, rl, p0, pend, ref, tau_delta=1e-3)
