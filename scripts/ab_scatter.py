@@ -37,15 +37,17 @@ for dist in ("zipf", "uniform"):
     for L in libs:
         assert call(L) == 0
     ev = {k: [] for k in range(len(libs))}
+    block = int(os.environ.get("BLOCK", "1"))   # consecutive calls of one library per round
     for r in range(rounds):
         for j in range(len(libs)):
             k = (j + r) % len(libs)
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            call(libs[k])
-            b.record()
-            ev[k].append((a, b))
+            for _ in range(block):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                call(libs[k])
+                b.record()
+                ev[k].append((a, b))
     torch.cuda.synchronize()
     for k, nm in enumerate(names):
         t = [a.elapsed_time(b) * 1e3 for a, b in ev[k]]
