@@ -660,7 +660,7 @@ __global__ void sc_validate(const int32_t* __restrict__ I, int64_t n, int64_t ro
 // Uniform indices thus stay one streaming pass, and a Zipf head row costs one
 // reduction per CTA instead of one per entry.
 constexpr int kHotSample = 4096;
-constexpr int kHotSampleHash = 8192;
+constexpr int kHotSampleHash = 8192;   // a multiple of the block size (warp-uniform candidate loop)
 constexpr int kHotHash = 1024;
 #ifndef PG_AH_HB
 #define PG_AH_HB 256
@@ -799,11 +799,17 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   // of them), ranked by (count desc, row asc) with a bitonic sort, so every
   // CTA derives the same ranking -- tier B's replica rows in global memory
   // must mean the same row in every CTA
-  for (int s2 = tid; s2 < kHotSampleHash; s2 += kThreads)
-    if (skey[s2] != -1 && scnt[s2] >= kHotMin) {
-      const int a = atomicAdd(&ncand, 1);
-      cand[a] = ((unsigned long long)(kHotSample - scnt[s2]) << 32) | (unsigned)skey[s2];
-    }
+  // (one shared-memory atomic per warp and pass: ~150 candidates taking a slot
+  // one atomic each were ~1.5 us of serialised atomics on one word)
+  for (int s2 = tid; s2 < kHotSampleHash; s2 += kThreads) {   // kHotSampleHash % kThreads == 0
+    const int key = skey[s2], ct = scnt[s2];
+    const bool take = key != -1 && ct >= kHotMin;
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    int base = 0;
+    if (lane == 0 && bal) base = atomicAdd(&ncand, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (take) cand[base + __popc(bal & ((1u << lane) - 1u))] = ((unsigned long long)(kHotSample - ct) << 32) | (unsigned)key;
+  }
   __syncthreads();
   const int nc = ncand;
   const int nh = nc < ha + hb ? nc : ha + hb;
@@ -814,7 +820,8 @@ __global__ void __launch_bounds__(kThreads, 1) sc_atomic_hot(const int32_t* __re
   for (int a = tid; a < nc; a += kThreads) {
     const unsigned long long key = cand[a];
     int rk = 0;
-    for (int b = 0; b < nc; ++b) rk += cand[b] < key;
+#pragma unroll 8
+    for (int b = 0; b < nc; ++b) rk += cand[b] < key;   // unrolled: 8 loads in flight
     if (rk < nh) {
       const int r = (int)(unsigned)(key & 0xffffffffull);
       hrow[rk] = r;

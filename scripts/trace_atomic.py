@@ -27,10 +27,16 @@ for dist in (sys.argv[1:] or ["zipf", "uniform"]):
     L.pg_debug_sort_trace(out.ctypes.data_as(ctypes.c_void_p))
     x = out[:148].astype(np.float64)
     t0 = x[:, 0].min()
-    names = ["start", "validated", "hotset", "bar.wait", "stream.end", "sync", "tierA.flush", "bar2", "end", "Wprefetch", "hashinit", "samplehash", "candsorted"]
+    names = ["start", "validated", "hotset", "bar.wait", "stream.end", "sync", "tierA.flush", "bar2", "end", "Wprefetch", "hashinit", "samplehash", "candsorted", "cand.own", "cand.sync"]
     print(dist)
     for k, nm in enumerate(names):
         col = np.where(x[:, k] > 0, (x[:, k] - t0) / 1e3, np.nan)
         if np.isnan(col).all():
             continue
         print(f"  {nm:11s} med {np.nanmedian(col):7.2f}  max {np.nanmax(col):7.2f} us")
+    last = out[:148, 15].astype(np.uint64)
+    if last.any():   # slot 15: the last warp to finish the candidate extraction (warp << 56 | time)
+        wl = (last >> np.uint64(56)).astype(int)
+        tl = (last & np.uint64((1 << 56) - 1)).astype(np.float64)
+        print("  last warp at the candidate barrier: warp ids", np.bincount(wl, minlength=32).nonzero()[0].tolist(),
+              f"med {np.median((tl - t0) / 1e3):.2f} us")
