@@ -15,7 +15,8 @@ cudart = ctypes.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64
 mb = float(sys.argv[1])
 import paper_1404_1521_b200 as pg
 rows, cols, N = 100_000, 64, 1_000_000
-I, Y = synth.scatter_inputs(rows, cols, N, "zipf", "random", seed=42)
+dist = os.environ.get("DIST", "zipf")
+I, Y = synth.scatter_inputs(rows, cols, N, dist, "random", seed=42)
 Id, Yd = torch.from_numpy(I).cuda(), torch.from_numpy(Y).cuda()
 W = torch.zeros(rows, cols, device="cuda")
 fl = torch.empty(128 * 1024 * 1024, device="cuda")
@@ -34,6 +35,6 @@ for _ in range(20):
     t.append((a, b))
 torch.cuda.synchronize()
 us = [a.elapsed_time(b) * 1e3 for a, b in t]
-print(f"dummy {mb:6.2f} MB: zipf atomic mean {statistics.mean(us):6.2f} us  median {statistics.median(us):6.2f}")
+print(f"dummy {mb:6.2f} MB: {dist} atomic mean {statistics.mean(us):6.2f} us  median {statistics.median(us):6.2f}")
 if os.environ.get("SHOW"):
     print("   per call:", " ".join(f"{x:.1f}" for x in us))
