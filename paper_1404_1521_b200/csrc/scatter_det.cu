@@ -399,7 +399,9 @@ __global__ void __launch_bounds__(kOT, 1) sc_det_owner(const int32_t* __restrict
       }
       key[j] = (dg << kOKeyBits) | (unsigned)i;
     }
+    OWN_MARK(14);
     o_pass<kOTagBits>(key, val, kOKeyBits, skeys, whA, dsA, ws);
+    OWN_MARK(15);
   }
   for (int o = tid; o < P; o += kOT) Hcnt[(size_t)c * P + o] = (unsigned)(dsA[o + 1] - dsA[o]);
   for (int h = tid; h < H; h += kOT) hmask[(size_t)c * kOHot + h] = dsA[P + h + 1] > dsA[P + h];

@@ -29,7 +29,7 @@ for dist in ([a for a in sys.argv[1:] if not a.startswith("--")] or ["zipf", "un
     L.pg_debug_owner_trace(out.ctypes.data_as(ctypes.c_void_p))
     x = out[:148].astype(np.float64)
     t0 = x[:, 0].min()
-    names = ["start", "A.hotset", "A.arrive", "H.sorted", "A.wait", "B.arrive", "C.start", "C.sorted", "C.end", "D.end", "A.loaded", "A.sampled", "B.Hload", "B.count"]
+    names = ["start", "A.hotset", "A.arrive", "H.sorted", "A.wait", "B.arrive", "C.start", "C.sorted", "C.end", "D.end", "A.loaded", "A.sampled", "B.Hload", "B.count", "A.tagged", "A.passed"]
     print(dist, "(no flush)" if noflush else "(L2 flushed)")
     for k, nm in enumerate(names):
         col = np.where(x[:, k] > 0, (x[:, k] - t0) / 1e3, np.nan)
