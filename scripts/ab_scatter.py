@@ -1,7 +1,12 @@
 """Same-process A/B of scatter-add variants: python scripts/ab_scatter.py MODE LIB [LIB ...]
 (LIB = 'main' for paper_1404_1521_b200/libpg.so, or a path from scripts/ab_variant.py).
 Every round runs each library once, in a rotating order, on the same buffers,
-L2 flushed before each call; prints the mean and median event time per library."""
+L2 flushed before each call; prints the mean and median event time per library.
+
+CAVEAT: each library instance allocates its own scratch, and the ATOMIC Zipf
+time depends on where that lands (76-88 us by placement), so
+the list position biases the comparison; compare one library per process at
+controlled placements instead (scripts/place_scan.py, PG_LIB_PATH)."""
 import ctypes
 import os
 import statistics
